@@ -1,0 +1,189 @@
+/*
+ * kvfuse_b200.h -- C ABI of the B200 (sm_100a) KV-block fusion library.
+ *
+ * This is the drop-in boundary for the reference's fusion hot path
+ * (/root/reference/pkg/src/kvfuse). The reference is pure Python/numpy; its
+ * "FFI" for this path is the Python call surface
+ *   fuse_batch  (fusion.py:360)   fuse_chunks (fusion.py:377)
+ *   fast_fusion (fusion.py:339)   refold      (core.py:285)
+ *   paged_attention (attention.py:58)
+ * which paper_2601_03067_b200/ mirrors and implements on top of the entry
+ * points below via ctypes (see INTEGRATION.md for the binding stub).
+ *
+ * Conventions
+ *  - Every pointer named *_dev / pool / norms / table ... is a DEVICE pointer
+ *    (cudaMalloc / torch CUDA storage). Host pointers are named *_host.
+ *  - `stream` is a cudaStream_t passed as void*. All entry points are
+ *    stream-ordered and asynchronous unless documented otherwise.
+ *  - dtype codes: 0 = float64, 1 = float32, 2 = bfloat16. "Acc" buffers
+ *    (norms, scales) are float64 for a float64 pool and float32 otherwise.
+ *  - Pool layout: (L, NB, t, h, d) C-order; NB = B*p physical blocks per
+ *    layer (reference cache (L, B, p, t, h, d), core.py:54-76). head_mode 0 =
+ *    "folded" (unit = layer; block vector = t*h*d entries, core.py:128),
+ *    1 = "per_head" (unit = layer*h + head; vector = t*d entries).
+ *  - Status codes: KVF_OK, or an error whose message kvf_last_error()
+ *    returns (thread-local). The Python layer maps them to the reference's
+ *    exception classes (errors.py:4-50).
+ */
+#ifndef KVFUSE_B200_H
+#define KVFUSE_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define KVF_OK 0
+#define KVF_ERR_INVALID 1    /* -> ConfigError / InvalidCacheError */
+#define KVF_ERR_ALIGNMENT 2  /* -> AlignmentError                  */
+#define KVF_ERR_CORRUPTION 3 /* -> CorruptionError                 */
+#define KVF_ERR_CUDA 4       /* CUDA runtime / launch failure      */
+
+#define KVF_PATH_AUTO 0
+#define KVF_PATH_SIMT 1  /* CUDA-core similarity (f64 / f32 / bf16)           */
+#define KVF_PATH_TC 2    /* tcgen05 + TMEM + TMA similarity (bf16 pools only) */
+
+/* Library identity and last error (thread-local). */
+const char* kvf_last_error(void);
+int kvf_version(void);
+
+/* Validation of a cache (PagedKvCache.__post_init__, core.py:73-74):
+ * adds the number of NaN/Inf entries of data[0:n] to *count_dev. */
+int kvf_count_nonfinite(const void* data, int dtype, int64_t n,
+                        unsigned long long* count_dev, void* stream);
+
+/* K1 -- per-block L2 norms (replaces _split_norm_direction, core.py:115-119).
+ * norms: Acc[U][NB], U = L (folded) or L*h (per_head). */
+int kvf_block_norms(const void* pool, int dtype, int64_t L, int64_t NB, int t,
+                    int h, int d, int head_mode, void* norms, void* stream);
+
+/* Fusion state for U units (replaces _Engine.__init__, fusion.py:208-228, and
+ * BlockTable.identity, core.py:191-201): fusable = knorm > 0, alive = 1,
+ * absorber = NONE, table = identity, refcount = 1. */
+int kvf_state_init(int dtype, int64_t U, int64_t NB, const void* knorm,
+                   uint8_t* fusable, uint8_t* alive, int32_t* absorber,
+                   int32_t* table, int32_t* refcount, void* stream);
+
+/* Similarity tile shape used by a path (tiles passed to
+ * kvf_similarity_select must be built with it). */
+int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
+                       int* tile_n);
+
+/* K2 + K3 -- similarity + first-match selection for every merge of one tree
+ * level (replaces fusion.py:244-265):
+ *   sim(i, j) = <x_i, x_j> / (|x_i| |x_j|) over alive, fusable blocks,
+ *   absorber[j] = min { i in left : sim(i, j) > thr }   (atomicMin).
+ * merges : int32[nm][3] block ranges {left_begin, split, right_end};
+ * tiles  : int32[nt][3] {merge, i0, j0} offsets inside the merge;
+ * partials (out): double[nU][nt][5] = {count, sum, sumsq, min, max} of sim;
+ * samples (optional, out): double, samples[(u-u0)*sample_stride +
+ *   sample_off[m] + il*right_n + jl] = sim or NaN for masked pairs. */
+int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
+                          int t, int h, int d, int head_mode, int64_t u0,
+                          int64_t nU, const void* knorm, const uint8_t* fusable,
+                          const uint8_t* alive, int32_t* absorber,
+                          const int32_t* merges, int nm, const int32_t* tiles,
+                          int nt, double thr, double* partials, double* samples,
+                          const int64_t* sample_off, int64_t sample_stride,
+                          int path, void* stream);
+
+/* Per-merge statistics of one level + absorber marking (MergeRecord,
+ * fusion.py:93-110, 273-281). stats: double[nU][nm][8] = {left_blocks,
+ * right_blocks, fused_count, n, sum, sumsq, min, max}. flag: int32[U][NB]
+ * scratch (zero on entry); list: int32 global ids u*NB+l of this level's
+ * absorbers, count_dev: int32[1] (zero on entry). */
+int kvf_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
+                    const uint8_t* alive, const int32_t* absorber,
+                    const int32_t* merges, int nm, const int32_t* tile_off,
+                    int nt, const double* partials, double* stats,
+                    int32_t* flag, int32_t* list, int32_t* count_dev,
+                    void* stream);
+
+/* K4 -- in-place block merge (replaces fusion.py:259-261, _unit 285-287):
+ * for each absorber l, dir = unit(dir_l + sum_{j: absorber[j]=l} dir_j) for K
+ * and the same indices for V; written back as s_home * dir with s_home the
+ * home slot's original norm (1 if zero), stored norm recomputed.
+ * row_merge: int32[rows] merge index of each row at this level (or -1). */
+int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L,
+                     int64_t NB, int t, int h, int d, int head_mode, void* knorm,
+                     void* vnorm, const void* orig_knorm, const void* orig_vnorm,
+                     const int32_t* absorber, const int32_t* merges,
+                     const int32_t* row_merge, int bpr, const int32_t* list,
+                     const int32_t* count_dev, int64_t list_cap, void* stream);
+
+/* K5 -- block-table remap + refcounts (replaces BlockTable.redirect,
+ * core.py:217-227, and alive[rid] = False, fusion.py:262-264). Clears flag. */
+int kvf_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber,
+              int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* flag,
+              void* stream);
+
+/* Finalize: per-slot scales k_scale[s] = orig_knorm[s] / knorm[table[s]]
+ * (same for V; refold semantics core.py:303-304), ascending live list
+ * (FusedLayer.phys_ids, fusion.py:316) and ascending free list per unit. */
+int kvf_finalize(int dtype, int64_t u0, int64_t nU, int64_t NB,
+                 const void* orig_knorm, const void* orig_vnorm,
+                 const void* knorm, const void* vnorm, const int32_t* table,
+                 const uint8_t* alive, void* k_scale, void* v_scale,
+                 int32_t* live_ids, int32_t* live_count, int32_t* free_ids,
+                 int32_t* free_count, void* stream);
+
+/* Device audit (BlockTable.audit, core.py:232-241): *bad_dev (int32, zeroed
+ * here) becomes nonzero if refcount != histogram(table), a slot points at a
+ * dead or out-of-range block, or a live block has refcount 0.
+ * scratch: int32[U*NB]. */
+int kvf_table_audit(int64_t U, int64_t NB, const int32_t* table,
+                    const int32_t* refcount, const uint8_t* alive,
+                    int32_t* scratch, int32_t* bad_dev, void* stream);
+
+/* BlockTable.redirect (core.py:217-227) for one unit; *bad_dev set when
+ * from/to is dangling. */
+int kvf_table_redirect(int64_t NB, int32_t* table, int32_t* refcount,
+                       uint8_t* alive, int32_t from_phys, int32_t to_phys,
+                       int32_t* bad_dev, void* stream);
+
+/* Gather vectors of unit u: out[k][:] = c_k * x_{ids[k]} (Acc dtype) with
+ * c_k = (norms ? 1/norms[u][ids[k]] : 1) * (scales ? scales[k] : 1).
+ * norms -> FusedLayer.directions (core.py:244-258); ids = table row and
+ * scales = k_scale row -> refold of one unit (core.py:298-304). */
+int kvf_gather_vectors(const void* pool, int dtype, int64_t L, int64_t NB,
+                       int t, int h, int d, int head_mode, int64_t u,
+                       const int32_t* ids, int64_t n, const void* norms,
+                       const void* scales, void* out, void* stream);
+
+/* refold (core.py:285-305) of one layer: out[s][tok][hh][:] =
+ * scale[u][s] * pool[layer][table[u][s]][tok][hh][:] with u = layer (folded)
+ * or layer*h + hh (per_head). out: Acc[NB][t][h][d]. */
+int kvf_refold(const void* pool, int dtype, int64_t L, int64_t NB, int t,
+               int h, int d, int head_mode, int64_t layer,
+               const int32_t* table, const void* scale, void* out,
+               void* stream);
+
+/* K6 -- paged decode attention over the fused cache (attention.py:58-80
+ * generalised to a batch, GQA and per-slot norm scales):
+ *   for request b, query head qh (kv head qh / (Hq/h)):
+ *   out = softmax(sm_scale * K q) V with K/V rows read through table/scales.
+ * q: Acc-or-bf16 [B][Hq][d] (q_dtype), out: float32 [B][Hq][d] (float64
+ * when dtype == 0), lse: same dtype [B][Hq], probs (optional, small
+ * problems): [B][Hq][p*t]. seq_blocks (optional) int32[B] valid blocks per
+ * request. workspace: kvf_decode_workspace_size() bytes. */
+int64_t kvf_decode_workspace_size(int dtype, int64_t B, int Hq, int d,
+                                  int64_t p_blocks, int t);
+int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
+                     const void* pool_v, int dtype, int64_t L, int64_t NB,
+                     int t, int h, int d, int head_mode, int64_t layer,
+                     const int32_t* table, const void* k_scale,
+                     const void* v_scale, int64_t B, int64_t p_blocks,
+                     const int32_t* seq_blocks, int Hq, double sm_scale,
+                     void* out, void* lse, void* probs, void* workspace,
+                     int64_t workspace_bytes, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVFUSE_B200_H */

@@ -1,0 +1,103 @@
+// Internal launch interface between the C ABI (kvf_abi.cu) and the kernel
+// translation units. Every launcher returns cudaGetLastError() of its launch.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include "common.cuh"
+
+namespace kvf {
+
+cudaError_t launch_count_nonfinite(const void* data, int dtype, int64_t n,
+                                   unsigned long long* count, cudaStream_t s);
+cudaError_t launch_block_norms(const void* pool, int dtype, const Geom& g,
+                               void* norms, cudaStream_t s);
+cudaError_t launch_state_init(int dtype, int64_t U, int64_t NB, const void* knorm,
+                              uint8_t* fusable, uint8_t* alive, int32_t* absorber,
+                              int32_t* table, int32_t* refcount, cudaStream_t s);
+
+struct SimArgs {
+  const void* pool;
+  int dtype;
+  Geom g;
+  int64_t u0, nU;
+  const void* knorm;
+  const uint8_t* fusable;
+  const uint8_t* alive;
+  int32_t* absorber;
+  const int32_t* merges;
+  int nm;
+  const int32_t* tiles;
+  int nt;
+  double thr;
+  double* partials;
+  double* samples;
+  const int64_t* sample_off;
+  int64_t sample_stride;
+};
+
+constexpr int kSimtTile = 64;
+cudaError_t launch_sim_simt(const SimArgs& a, cudaStream_t s);
+
+// tcgen05 path (bf16 only): tile 128 x kTcTileN
+constexpr int kTcTileM = 128;
+constexpr int kTcTileN = 256;
+bool tc_supported(const SimArgs& a, const char** why);
+cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s);
+
+cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
+                               const uint8_t* alive, const int32_t* absorber,
+                               const int32_t* merges, int nm, const int32_t* tile_off,
+                               int nt, const double* partials, double* stats,
+                               int32_t* flag, int32_t* list, int32_t* count, cudaStream_t s);
+cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
+                                void* knorm, void* vnorm, const void* oknorm,
+                                const void* ovnorm, const int32_t* absorber,
+                                const int32_t* merges, const int32_t* row_merge, int bpr,
+                                const int32_t* list, const int32_t* count, int64_t cap,
+                                cudaStream_t s);
+cudaError_t launch_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber,
+                         int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* flag,
+                         cudaStream_t s);
+cudaError_t launch_finalize(int dtype, int64_t u0, int64_t nU, int64_t NB, const void* okn,
+                            const void* ovn, const void* kn, const void* vn,
+                            const int32_t* table, const uint8_t* alive, void* ks, void* vs,
+                            int32_t* live_ids, int32_t* live_count, int32_t* free_ids,
+                            int32_t* free_count, cudaStream_t s);
+cudaError_t launch_table_audit(int64_t U, int64_t NB, const int32_t* table,
+                               const int32_t* refcount, const uint8_t* alive,
+                               int32_t* scratch, int32_t* bad, cudaStream_t s);
+cudaError_t launch_table_redirect(int64_t NB, int32_t* table, int32_t* refcount,
+                                  uint8_t* alive, int32_t from, int32_t to, int32_t* bad,
+                                  cudaStream_t s);
+cudaError_t launch_gather_vectors(const void* pool, int dtype, const Geom& g, int64_t u,
+                                  const int32_t* ids, int64_t n, const void* norms,
+                                  const void* scales, void* out, cudaStream_t s);
+cudaError_t launch_refold(const void* pool, int dtype, const Geom& g, int64_t layer,
+                          const int32_t* table, const void* scale, void* out,
+                          cudaStream_t s);
+
+int64_t decode_workspace_size(int dtype, int64_t B, int Hq, int d, int64_t p_blocks, int t);
+struct DecodeArgs {
+  const void* q;
+  int q_dtype;
+  const void* pool_k;
+  const void* pool_v;
+  int dtype;
+  Geom g;
+  int64_t layer;
+  const int32_t* table;
+  const void* k_scale;
+  const void* v_scale;
+  int64_t B, p_blocks;
+  const int32_t* seq_blocks;
+  int Hq;
+  double sm_scale;
+  void* out;
+  void* lse;
+  void* probs;
+  void* ws;
+  int64_t ws_bytes;
+};
+cudaError_t launch_paged_decode(const DecodeArgs& a, cudaStream_t s);
+
+}  // namespace kvf

@@ -1,0 +1,287 @@
+// extern "C" boundary of libkvfuse_b200.so (declared in include/kvfuse_b200.h).
+// Validates arguments, dispatches to the kernel launchers, and maps failures
+// to status codes + a thread-local message (kvf_last_error).
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include "../../include/kvfuse_b200.h"
+#include "kernels.h"
+
+using namespace kvf;
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return KVF_OK;
+  return fail(KVF_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+bool valid_dtype(int dt) { return dt == F64 || dt == F32 || dt == BF16; }
+
+int check_geom(int64_t L, int64_t NB, int t, int h, int d, int head_mode, Geom* g) {
+  if (L < 1 || NB < 1 || t < 1 || h < 1 || d < 1)
+    return fail(KVF_ERR_INVALID, "dimensions must be positive (L=%lld NB=%lld t=%d h=%d d=%d)",
+                (long long)L, (long long)NB, t, h, d);
+  if (head_mode != 0 && head_mode != 1)
+    return fail(KVF_ERR_INVALID, "head_mode must be 0 (folded) or 1 (per_head)");
+  if (NB >= (int64_t)INT32_MAX / 2)
+    return fail(KVF_ERR_INVALID, "too many blocks per layer (%lld)", (long long)NB);
+  g->L = L;
+  g->NB = NB;
+  g->t = t;
+  g->h = h;
+  g->d = d;
+  g->head_mode = head_mode;
+  if (g->units() * NB >= (int64_t)INT32_MAX)
+    return fail(KVF_ERR_INVALID, "units*blocks exceeds int32 ids");
+  return KVF_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* kvf_last_error(void) { return g_last_error.c_str(); }
+int kvf_version(void) { return 10000; }
+
+int kvf_count_nonfinite(const void* data, int dtype, int64_t n, unsigned long long* count_dev,
+                        void* stream) {
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (n > 0 && (!data || !count_dev)) return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_count_nonfinite(data, dtype, n, count_dev, (cudaStream_t)stream),
+                     "kvf_count_nonfinite");
+}
+
+int kvf_block_norms(const void* pool, int dtype, int64_t L, int64_t NB, int t, int h, int d,
+                    int head_mode, void* norms, void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (!pool || !norms) return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_block_norms(pool, dtype, g, norms, (cudaStream_t)stream),
+                     "kvf_block_norms");
+}
+
+int kvf_state_init(int dtype, int64_t U, int64_t NB, const void* knorm, uint8_t* fusable,
+                   uint8_t* alive, int32_t* absorber, int32_t* table, int32_t* refcount,
+                   void* stream) {
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (U < 0 || NB < 0) return fail(KVF_ERR_INVALID, "negative sizes");
+  return cuda_status(launch_state_init(dtype, U, NB, knorm, fusable, alive, absorber, table,
+                                       refcount, (cudaStream_t)stream),
+                     "kvf_state_init");
+}
+
+int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m, int* tile_n) {
+  if (!tile_m || !tile_n) return fail(KVF_ERR_INVALID, "null pointer");
+  if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
+  if (path == KVF_PATH_TC) {
+    if (dtype != BF16) return fail(KVF_ERR_INVALID, "tcgen05 path requires a bf16 pool");
+    *tile_m = kTcTileM;
+    *tile_n = kTcTileN;
+    return KVF_OK;
+  }
+  if (path != KVF_PATH_SIMT) return fail(KVF_ERR_INVALID, "unknown path %d", path);
+  *tile_m = kSimtTile;
+  *tile_n = kSimtTile;
+  return KVF_OK;
+}
+
+int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, int t, int h,
+                          int d, int head_mode, int64_t u0, int64_t nU, const void* knorm,
+                          const uint8_t* fusable, const uint8_t* alive, int32_t* absorber,
+                          const int32_t* merges, int nm, const int32_t* tiles, int nt,
+                          double thr, double* partials, double* samples,
+                          const int64_t* sample_off, int64_t sample_stride, int path,
+                          void* stream) {
+  SimArgs a;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (!(thr > -1.0 && thr < 1.0))
+    return fail(KVF_ERR_INVALID, "threshold must lie strictly inside (-1, 1), got %g", thr);
+  if (u0 < 0 || nU < 0 || u0 + nU > a.g.units())
+    return fail(KVF_ERR_INVALID, "unit range [%lld, %lld) out of bounds", (long long)u0,
+                (long long)(u0 + nU));
+  if (nt > 0 && (!pool_k || !knorm || !fusable || !alive || !absorber || !merges || !tiles ||
+                 !partials))
+    return fail(KVF_ERR_INVALID, "null pointer");
+  if (samples && !sample_off) return fail(KVF_ERR_INVALID, "samples need sample_off");
+  a.pool = pool_k;
+  a.dtype = dtype;
+  a.u0 = u0;
+  a.nU = nU;
+  a.knorm = knorm;
+  a.fusable = fusable;
+  a.alive = alive;
+  a.absorber = absorber;
+  a.merges = merges;
+  a.nm = nm;
+  a.tiles = tiles;
+  a.nt = nt;
+  a.thr = thr;
+  a.partials = partials;
+  a.samples = samples;
+  a.sample_off = sample_off;
+  a.sample_stride = sample_stride;
+  if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
+  if (path == KVF_PATH_TC) {
+    const char* why = "";
+    if (!tc_supported(a, &why))
+      return fail(KVF_ERR_INVALID, "tcgen05 similarity path unavailable: %s", why);
+    return cuda_status(launch_sim_tc(a, (cudaStream_t)stream), "kvf_similarity_select[tc]");
+  }
+  if (path != KVF_PATH_SIMT) return fail(KVF_ERR_INVALID, "unknown path %d", path);
+  return cuda_status(launch_sim_simt(a, (cudaStream_t)stream), "kvf_similarity_select[simt]");
+}
+
+int kvf_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
+                    const uint8_t* alive, const int32_t* absorber, const int32_t* merges, int nm,
+                    const int32_t* tile_off, int nt, const double* partials, double* stats,
+                    int32_t* flag, int32_t* list, int32_t* count_dev, void* stream) {
+  if (nm > 0 && nU > 0 && (!fusable || !alive || !absorber || !merges || !tile_off || !stats ||
+                           !flag || !list || !count_dev))
+    return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_level_stats(u0, nU, NB, fusable, alive, absorber, merges, nm,
+                                        tile_off, nt, partials, stats, flag, list, count_dev,
+                                        (cudaStream_t)stream),
+                     "kvf_level_stats");
+}
+
+int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t NB, int t, int h,
+                     int d, int head_mode, void* knorm, void* vnorm, const void* orig_knorm,
+                     const void* orig_vnorm, const int32_t* absorber, const int32_t* merges,
+                     const int32_t* row_merge, int bpr, const int32_t* list,
+                     const int32_t* count_dev, int64_t list_cap, void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (bpr < 1) return fail(KVF_ERR_INVALID, "bpr must be >= 1");
+  const int64_t r = g.r();
+  const int64_t rmax = dtype == F64 ? 16384 : 32768;
+  if (r > rmax)
+    return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's %lld",
+                (long long)r, (long long)rmax);
+  cudaError_t e = launch_merge_groups(pool_k, pool_v, dtype, g, knorm, vnorm, orig_knorm,
+                                      orig_vnorm, absorber, merges, row_merge, bpr, list,
+                                      count_dev, list_cap, (cudaStream_t)stream);
+  return cuda_status(e, "kvf_merge_groups");
+}
+
+int kvf_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber, int32_t* table,
+              int32_t* refcount, uint8_t* alive, int32_t* flag, void* stream) {
+  return cuda_status(
+      launch_remap(u0, nU, NB, absorber, table, refcount, alive, flag, (cudaStream_t)stream),
+      "kvf_remap");
+}
+
+int kvf_finalize(int dtype, int64_t u0, int64_t nU, int64_t NB, const void* orig_knorm,
+                 const void* orig_vnorm, const void* knorm, const void* vnorm,
+                 const int32_t* table, const uint8_t* alive, void* k_scale, void* v_scale,
+                 int32_t* live_ids, int32_t* live_count, int32_t* free_ids, int32_t* free_count,
+                 void* stream) {
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  return cuda_status(launch_finalize(dtype, u0, nU, NB, orig_knorm, orig_vnorm, knorm, vnorm,
+                                     table, alive, k_scale, v_scale, live_ids, live_count,
+                                     free_ids, free_count, (cudaStream_t)stream),
+                     "kvf_finalize");
+}
+
+int kvf_table_audit(int64_t U, int64_t NB, const int32_t* table, const int32_t* refcount,
+                    const uint8_t* alive, int32_t* scratch, int32_t* bad_dev, void* stream) {
+  if (!bad_dev) return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_table_audit(U, NB, table, refcount, alive, scratch, bad_dev,
+                                        (cudaStream_t)stream),
+                     "kvf_table_audit");
+}
+
+int kvf_table_redirect(int64_t NB, int32_t* table, int32_t* refcount, uint8_t* alive,
+                       int32_t from_phys, int32_t to_phys, int32_t* bad_dev, void* stream) {
+  if (!table || !refcount || !alive || !bad_dev) return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_table_redirect(NB, table, refcount, alive, from_phys, to_phys,
+                                           bad_dev, (cudaStream_t)stream),
+                     "kvf_table_redirect");
+}
+
+int kvf_gather_vectors(const void* pool, int dtype, int64_t L, int64_t NB, int t, int h, int d,
+                       int head_mode, int64_t u, const int32_t* ids, int64_t n,
+                       const void* norms, const void* scales, void* out, void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (u < 0 || u >= g.units()) return fail(KVF_ERR_INVALID, "unit %lld out of range", (long long)u);
+  return cuda_status(
+      launch_gather_vectors(pool, dtype, g, u, ids, n, norms, scales, out, (cudaStream_t)stream),
+      "kvf_gather_vectors");
+}
+
+int kvf_refold(const void* pool, int dtype, int64_t L, int64_t NB, int t, int h, int d,
+               int head_mode, int64_t layer, const int32_t* table, const void* scale, void* out,
+               void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
+  if (layer < 0 || layer >= L)
+    return fail(KVF_ERR_INVALID, "layer %lld out of range [0, %lld)", (long long)layer,
+                (long long)L);
+  return cuda_status(launch_refold(pool, dtype, g, layer, table, scale, out, (cudaStream_t)stream),
+                     "kvf_refold");
+}
+
+int64_t kvf_decode_workspace_size(int dtype, int64_t B, int Hq, int d, int64_t p_blocks, int t) {
+  return decode_workspace_size(dtype, B, Hq, d, p_blocks, t);
+}
+
+int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k, const void* pool_v,
+                     int dtype, int64_t L, int64_t NB, int t, int h, int d, int head_mode,
+                     int64_t layer, const int32_t* table, const void* k_scale,
+                     const void* v_scale, int64_t B, int64_t p_blocks,
+                     const int32_t* seq_blocks, int Hq, double sm_scale, void* out, void* lse,
+                     void* probs, void* workspace, int64_t workspace_bytes, void* stream) {
+  DecodeArgs a;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
+  if (!valid_dtype(dtype) || !valid_dtype(q_dtype)) return fail(KVF_ERR_INVALID, "bad dtype");
+  if (layer < 0 || layer >= L) return fail(KVF_ERR_INVALID, "layer out of range");
+  if (Hq < 1 || Hq % h != 0)
+    return fail(KVF_ERR_INVALID, "query heads %d must be a positive multiple of kv heads %d", Hq, h);
+  if (Hq / h > 8 || d > 128 || t > 32)
+    return fail(KVF_ERR_INVALID, "decode kernel limits: Hq/h <= 8, d <= 128, t <= 32");
+  if (B < 0 || p_blocks < 1 || B * p_blocks > NB)
+    return fail(KVF_ERR_INVALID, "B*p_blocks (%lld) exceeds blocks per layer (%lld)",
+                (long long)(B * p_blocks), (long long)NB);
+  a.q = q;
+  a.q_dtype = q_dtype;
+  a.pool_k = pool_k;
+  a.pool_v = pool_v;
+  a.dtype = dtype;
+  a.layer = layer;
+  a.table = table;
+  a.k_scale = k_scale;
+  a.v_scale = v_scale;
+  a.B = B;
+  a.p_blocks = p_blocks;
+  a.seq_blocks = seq_blocks;
+  a.Hq = Hq;
+  a.sm_scale = sm_scale;
+  a.out = out;
+  a.lse = lse;
+  a.probs = probs;
+  a.ws = workspace;
+  a.ws_bytes = workspace_bytes;
+  if (workspace_bytes < decode_workspace_size(dtype, B, Hq, d, p_blocks, t))
+    return fail(KVF_ERR_INVALID, "decode workspace too small");
+  return cuda_status(launch_paged_decode(a, (cudaStream_t)stream), "kvf_paged_decode");
+}
+
+}  // extern "C"

@@ -1,0 +1,303 @@
+"""Device fusion engine: runs the merge tree level by level on the GPU.
+
+One `FusionState` holds the fusion state of U independent units that share a
+merge plan (all layers -- and, in per-head mode, all KV heads -- of a cache).
+Per tree level the engine issues four stream-ordered launches:
+
+  kvf_similarity_select  K2+K3  similarity GEMM + first-match epilogue
+  kvf_level_stats               MergeRecord counters + absorber marking
+  kvf_merge_groups       K4     normalised-sum merge, written in place
+  kvf_remap              K5     block table / refcount / alive update
+
+and `kvf_finalize` afterwards derives per-slot K/V scales and the ascending
+live / free block lists. Reference: _Engine (fusion.py:205-282) and
+_fuse_layer (fusion.py:290-336), restated level-synchronously.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError
+from .schedule import Plan
+
+NONE = 0x7FFFFFFF
+
+_DT = {torch.float64: N.DT_F64, torch.float32: N.DT_F32, torch.bfloat16: N.DT_BF16}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _DT[dt]
+    except KeyError:
+        raise ConfigError(f"unsupported pool dtype {dt}; use float64, float32 or bfloat16") from None
+
+
+def acc_dtype(dt: torch.dtype) -> torch.dtype:
+    return torch.float64 if dt == torch.float64 else torch.float32
+
+
+@dataclass(frozen=True)
+class Geometry:
+    """Pool (L, NB, t, h, d) and unit layout."""
+
+    L: int
+    NB: int
+    t: int
+    h: int
+    d: int
+    head_mode: int = 0  # 0 folded (unit = layer), 1 per_head (unit = layer*h + head)
+
+    @property
+    def units(self) -> int:
+        return self.L * self.h if self.head_mode else self.L
+
+    @property
+    def r(self) -> int:
+        return self.t * self.d if self.head_mode else self.t * self.h * self.d
+
+    @property
+    def E(self) -> int:
+        return self.t * self.h * self.d
+
+    def args(self):
+        return (self.L, self.NB, self.t, self.h, self.d, self.head_mode)
+
+
+def block_norms(pool: torch.Tensor, geom: Geometry, stream=None) -> torch.Tensor:
+    """K1: per-(unit, block) L2 norms, Acc[U, NB] (core.py:115-119)."""
+    out = torch.empty((geom.units, geom.NB), dtype=acc_dtype(pool.dtype), device=pool.device)
+    N.call(
+        "kvf_block_norms", N.ptr(pool), dtype_code(pool.dtype), *geom.args(), N.ptr(out),
+        N.stream_ptr(stream),
+    )
+    return out
+
+
+class _PlanDevice:
+    """Device copies of one plan's per-level arrays (uploaded once)."""
+
+    def __init__(self, plan: Plan, tm: int, tn: int, device):
+        self.levels = []
+        for lv in plan.levels:
+            tiles, tile_off = lv.tiling(tm, tn)
+            rect = lv.rect_sizes()
+            s_off = np.concatenate([[0], np.cumsum(rect)[:-1]]).astype(np.int64)
+            self.levels.append(
+                dict(
+                    merges=torch.from_numpy(lv.merges.copy()).to(device),
+                    row_merge=torch.from_numpy(lv.row_merge.copy()).to(device),
+                    tiles=torch.from_numpy(tiles.copy()).to(device),
+                    tile_off=torch.from_numpy(tile_off.copy()).to(device),
+                    sample_off=torch.from_numpy(s_off).to(device),
+                    nm=int(lv.merges.shape[0]),
+                    nt=int(tiles.shape[0]),
+                    rect_total=int(rect.sum()),
+                )
+            )
+
+
+def _plan_device(plan: Plan, tm: int, tn: int, device) -> _PlanDevice:
+    cache = plan.__dict__.setdefault("_device_cache", {})
+    key = (tm, tn, str(device))
+    if key not in cache:
+        cache[key] = _PlanDevice(plan, tm, tn, device)
+    return cache[key]
+
+
+def tile_shape(dtype: torch.dtype, head_mode: int, path: int) -> tuple[int, int]:
+    import ctypes as C
+
+    tm, tn = C.c_int(), C.c_int()
+    N.call("kvf_sim_tile_shape", dtype_code(dtype), head_mode, path, C.byref(tm), C.byref(tn))
+    return tm.value, tn.value
+
+
+@dataclass
+class FusionState:
+    """Device-resident result of fusing U units (all tensors [U, NB] unless noted)."""
+
+    geom: Geometry
+    plan: Plan
+    threshold: float
+    pool_k: torch.Tensor
+    pool_v: torch.Tensor
+    knorm: torch.Tensor  # stored norms of the (possibly rewritten) pool blocks
+    vnorm: torch.Tensor
+    orig_knorm: torch.Tensor  # per-slot original norms (FusedCache.key_norms)
+    orig_vnorm: torch.Tensor
+    fusable: torch.Tensor
+    alive: torch.Tensor
+    absorber: torch.Tensor  # event record: absorber[j] = l (or NONE)
+    table: torch.Tensor  # slot -> physical block
+    refcount: torch.Tensor
+    k_scale: torch.Tensor | None = None
+    v_scale: torch.Tensor | None = None
+    live_ids: torch.Tensor | None = None
+    live_count: torch.Tensor | None = None  # [U]
+    free_ids: torch.Tensor | None = None
+    free_count: torch.Tensor | None = None
+    level_stats: list[torch.Tensor] = field(default_factory=list)  # per level [U, nm, 8]
+    level_samples: list[torch.Tensor | None] = field(default_factory=list)
+    launches: int = 0
+    sim_events: list = field(default_factory=list)  # (start, end, level) CUDA events
+
+
+class FusionEngine:
+    """Runs fusion of all units of a geometry for one plan (see module doc)."""
+
+    def __init__(self, geom: Geometry, plan: Plan, dtype: torch.dtype, device, path: int = N.PATH_AUTO):
+        if plan.n_blocks != geom.NB:
+            raise ConfigError(f"plan covers {plan.n_blocks} blocks, geometry has {geom.NB}")
+        self.geom = geom
+        self.plan = plan
+        self.dtype = dtype
+        self.device = torch.device(device)
+        if path == N.PATH_AUTO:
+            path = N.PATH_TC if dtype == torch.bfloat16 and tc_available(geom) else N.PATH_SIMT
+        self.path = path
+        self.tm, self.tn = tile_shape(dtype, geom.head_mode, path)
+        self.pdev = _plan_device(plan, self.tm, self.tn, self.device)
+        U, NB = geom.units, geom.NB
+        dev = self.device
+        max_nt = max([lv["nt"] for lv in self.pdev.levels], default=1)
+        self.partials = torch.empty((U, max(max_nt, 1), 5), dtype=torch.float64, device=dev)
+        self.flag = torch.zeros(U * NB, dtype=torch.int32, device=dev)
+        self.list = torch.empty(U * NB, dtype=torch.int32, device=dev)
+        self.count = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def run(
+        self,
+        pool_k: torch.Tensor,
+        pool_v: torch.Tensor,
+        threshold: float,
+        *,
+        orig_knorm: torch.Tensor | None = None,
+        orig_vnorm: torch.Tensor | None = None,
+        table: torch.Tensor | None = None,
+        refcount: torch.Tensor | None = None,
+        alive: torch.Tensor | None = None,
+        keep_samples: bool = False,
+        time_sim: bool = False,
+        stream=None,
+    ) -> FusionState:
+        g, dev = self.geom, self.device
+        if not -1.0 < threshold < 1.0:
+            raise ConfigError(f"threshold must lie strictly inside (-1, 1), got {threshold}")
+        if pool_k.dtype != self.dtype or pool_v.dtype != self.dtype:
+            raise ConfigError("pool dtype does not match the engine")
+        if pool_k.numel() != g.L * g.NB * g.E or pool_v.numel() != pool_k.numel():
+            raise ConfigError("pool size does not match the geometry")
+        if not (pool_k.is_contiguous() and pool_v.is_contiguous()):
+            raise ConfigError("pools must be contiguous")
+        sp = N.stream_ptr(stream)
+        dt = dtype_code(self.dtype)
+        U, NB = g.units, g.NB
+        acc = acc_dtype(self.dtype)
+        launches = 0
+        knorm = block_norms(pool_k, g, stream)
+        vnorm = block_norms(pool_v, g, stream)
+        launches += 2
+        oknorm = knorm.clone() if orig_knorm is None else orig_knorm.reshape(U, NB).to(acc)
+        ovnorm = vnorm.clone() if orig_vnorm is None else orig_vnorm.reshape(U, NB).to(acc)
+        fusable = torch.empty((U, NB), dtype=torch.uint8, device=dev)
+        alive_t = torch.empty((U, NB), dtype=torch.uint8, device=dev) if alive is None else alive
+        absorber = torch.empty((U, NB), dtype=torch.int32, device=dev)
+        table_t = torch.empty((U, NB), dtype=torch.int32, device=dev) if table is None else table
+        ref_t = torch.empty((U, NB), dtype=torch.int32, device=dev) if refcount is None else refcount
+        N.call(
+            "kvf_state_init", dt, U, NB, N.ptr(oknorm), N.ptr(fusable), N.ptr(alive_t),
+            N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t), sp,
+        )
+        launches += 1
+        st = FusionState(
+            g, self.plan, threshold, pool_k, pool_v, knorm, vnorm, oknorm, ovnorm, fusable,
+            alive_t, absorber, table_t, ref_t,
+        )
+        self.flag.zero_()
+        for li, lv in enumerate(self.pdev.levels):
+            nm, nt = lv["nm"], lv["nt"]
+            stats = torch.empty((U, nm, 8), dtype=torch.float64, device=dev)
+            samples = None
+            if keep_samples:
+                samples = torch.empty((U, max(lv["rect_total"], 1)), dtype=torch.float64, device=dev)
+            if time_sim:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            N.call(
+                "kvf_similarity_select", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(knorm),
+                N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber), N.ptr(lv["merges"]), nm,
+                N.ptr(lv["tiles"]), nt, float(threshold), N.ptr(self.partials), N.ptr(samples),
+                N.ptr(lv["sample_off"]) if samples is not None else None,
+                samples.shape[1] if samples is not None else 0, self.path, sp,
+            )
+            if time_sim:
+                e1.record(stream)
+                st.sim_events.append((e0, e1, li))
+            self.count.zero_()
+            N.call(
+                "kvf_level_stats", 0, U, NB, N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber),
+                N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off"]), nt, N.ptr(self.partials),
+                N.ptr(stats), N.ptr(self.flag), N.ptr(self.list), N.ptr(self.count), sp,
+            )
+            N.call(
+                "kvf_merge_groups", N.ptr(pool_k), N.ptr(pool_v), dt, *g.args(), N.ptr(knorm),
+                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(absorber), N.ptr(lv["merges"]),
+                N.ptr(lv["row_merge"]), self.plan.bpr, N.ptr(self.list), N.ptr(self.count),
+                U * NB, sp,
+            )
+            N.call(
+                "kvf_remap", 0, U, NB, N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t),
+                N.ptr(alive_t), N.ptr(self.flag), sp,
+            )
+            launches += 4
+            st.level_stats.append(stats)
+            st.level_samples.append(samples)
+        st.k_scale = torch.empty((U, NB), dtype=acc, device=dev)
+        st.v_scale = torch.empty((U, NB), dtype=acc, device=dev)
+        st.live_ids = torch.empty((U, NB), dtype=torch.int32, device=dev)
+        st.free_ids = torch.empty((U, NB), dtype=torch.int32, device=dev)
+        st.live_count = torch.empty(U, dtype=torch.int32, device=dev)
+        st.free_count = torch.empty(U, dtype=torch.int32, device=dev)
+        N.call(
+            "kvf_finalize", dt, 0, U, NB, N.ptr(oknorm), N.ptr(ovnorm), N.ptr(knorm),
+            N.ptr(vnorm), N.ptr(table_t), N.ptr(alive_t), N.ptr(st.k_scale), N.ptr(st.v_scale),
+            N.ptr(st.live_ids), N.ptr(st.live_count), N.ptr(st.free_ids), N.ptr(st.free_count),
+            sp,
+        )
+        launches += 2
+        st.launches = launches
+        return st
+
+
+def tc_available(geom: Geometry) -> bool:
+    """Whether the tcgen05 similarity path accepts this geometry (bf16 pools)."""
+    try:
+        tm, tn = tile_shape(torch.bfloat16, geom.head_mode, N.PATH_TC)
+    except Exception:
+        return False
+    return _tc_geometry_ok(geom)
+
+
+def _tc_geometry_ok(geom: Geometry) -> bool:
+    # TMA tiles are 64-element (128 B) slices of the head dim
+    return geom.d % 64 == 0 and _TC_ENABLED
+
+
+_TC_ENABLED = False
+
+
+def audit(table: torch.Tensor, refcount: torch.Tensor, alive: torch.Tensor, U: int, NB: int) -> bool:
+    """Device BlockTable.audit (core.py:232-241); True when consistent."""
+    scratch = torch.empty(max(U * NB, 1), dtype=torch.int32, device=table.device)
+    bad = torch.empty(1, dtype=torch.int32, device=table.device)
+    N.call(
+        "kvf_table_audit", U, NB, N.ptr(table), N.ptr(refcount), N.ptr(alive), N.ptr(scratch),
+        N.ptr(bad), N.stream_ptr(),
+    )
+    return int(bad.item()) == 0

@@ -1,0 +1,62 @@
+"""Deterministic synthetic KV caches, generated on the GPU.
+
+Mirrors the structure of the reference generator (workload.py:144-171:
+clustered block directions, K and V sharing the cluster assignment,
+lognormal(0, 0.25) block norms) but replaces its Monte-Carlo noise
+calibration (workload.py:89-125, minutes at r = 16,384) with the closed form
+sigma_b = sqrt((1/c^2 - 1) / r), which puts each block at cosine c from its
+cluster centre; c ~ U[c_lo, c_hi] per block. Test / bench infrastructure.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+
+def _layer_blocks(gen: torch.Generator, n: int, r: int, assign: torch.Tensor, n_clusters: int,
+                  c_lo: float, c_hi: float, device) -> torch.Tensor:
+    bases = torch.randn((n_clusters, r), generator=gen, device=device)
+    bases = bases / bases.norm(dim=1, keepdim=True)
+    c = c_lo + (c_hi - c_lo) * torch.rand((n, 1), generator=gen, device=device)
+    sigma = torch.sqrt((1.0 / (c * c) - 1.0) / r)
+    x = bases[assign] + sigma * torch.randn((n, r), generator=gen, device=device)
+    x = x / x.norm(dim=1, keepdim=True)
+    norms = torch.exp(0.25 * torch.randn((n, 1), generator=gen, device=device))
+    return x * norms
+
+
+def synthetic_kv(L: int, B: int, p: int, t: int, h: int, d: int, *, dtype=torch.bfloat16,
+                 seed: int = 0, variant: str = "bff", c_lo: float = 0.80, c_hi: float = 0.99,
+                 cluster_div: int = 4, device=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """K, V of shape (L, B, p, t, h, d). BFF: B*p/4 clusters per layer shared
+    across requests; CFF: p/4 clusters per request (chunks of one request)."""
+    device = torch.device(device or "cuda")
+    r = t * h * d
+    n = B * p
+    K = torch.empty((L, B, p, t, h, d), dtype=dtype, device=device)
+    V = torch.empty_like(K)
+    for layer in range(L):
+        gen = torch.Generator(device=device)
+        gen.manual_seed((seed * 1_000_003 + layer * 7919) & 0x7FFF_FFFF_FFFF)
+        if variant == "bff":
+            nc = max(1, n // cluster_div)
+            assign = torch.randint(0, nc, (n,), generator=gen, device=device)
+        else:
+            per = max(1, p // cluster_div)
+            nc = per * B
+            assign = (torch.randint(0, per, (B, p), generator=gen, device=device)
+                      + torch.arange(B, device=device)[:, None] * per).reshape(-1)
+        for out in (K, V):
+            blk = _layer_blocks(gen, n, r, assign, nc, c_lo, c_hi, device)
+            out[layer].copy_(blk.reshape(B, p, t, h, d).to(dtype))
+    return K, V
+
+
+def kv_bytes(L: int, B: int, p: int, t: int, h: int, d: int, dtype: torch.dtype) -> int:
+    return 2 * L * B * p * t * h * d * torch.empty(0, dtype=dtype).element_size()
+
+
+def noise_sigma(c: float, r: int) -> float:
+    return math.sqrt((1.0 / (c * c) - 1.0) / r)
