@@ -80,7 +80,14 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
  * tiles  : int32[nt][3] {merge, i0, j0} offsets inside the merge;
  * partials (out): double[nU][nt][5] = {count, sum, sumsq, min, max} of sim;
  * samples (optional, out): double, samples[(u-u0)*sample_stride +
- *   sample_off[m] + il*right_n + jl] = sim or NaN for masked pairs. */
+ *   sample_off[m] + il*right_n + jl] = sim or NaN for masked pairs (compacted
+ *   launches leave dead pairs untouched: pre-fill with NaN).
+ * Compaction (tcgen05 path only; all three or none): live/rank from
+ * kvf_alive_rank and staged from kvf_stage_rows -- tiles then index the
+ * merge's alive blocks only and operands stream from the staged rows.
+ * Re-score (tcgen05 path): pairs with |sim - thr| <= rescore_band are queued
+ * (int32[4 * (rescore_cap + 1)], entries then the count) and decided from a
+ * float64 recomputation in the same call; NULL / 0 disables it. */
 int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           int t, int h, int d, int head_mode, int64_t u0,
                           int64_t nU, const void* knorm, const uint8_t* fusable,
@@ -88,7 +95,22 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           const int32_t* merges, int nm, const int32_t* tiles,
                           int nt, double thr, double* partials, double* samples,
                           const int64_t* sample_off, int64_t sample_stride,
-                          int path, void* stream);
+                          const int32_t* live, const int32_t* rank,
+                          const void* staged, int32_t* rescore_queue,
+                          int64_t rescore_cap, double rescore_band, int path,
+                          void* stream);
+
+/* Ascending alive list live[U][NB], exclusive rank[U][NB + 1] (number of
+ * alive blocks before each id) and count[U] for units [u0, u0 + nU). */
+int kvf_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive,
+                   int32_t* live, int32_t* rank, int32_t* count, void* stream);
+
+/* Staged copy of the alive K rows: staged[(u - u0) * NB + k][0:r] =
+ * vector(u, live[u][k]) for k < count[u] (bf16 pools). */
+int kvf_stage_rows(const void* pool, int dtype, int64_t L, int64_t NB, int t,
+                   int h, int d, int head_mode, int64_t u0, int64_t nU,
+                   const int32_t* live, const int32_t* count, void* staged,
+                   void* stream);
 
 /* Per-merge statistics of one level + absorber marking (MergeRecord,
  * fusion.py:93-110, 273-281). stats: double[nU][nm][8] = {left_blocks,
@@ -106,13 +128,19 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
  * for each absorber l, dir = unit(dir_l + sum_{j: absorber[j]=l} dir_j) for K
  * and the same indices for V; written back as s_home * dir with s_home the
  * home slot's original norm (1 if zero), stored norm recomputed.
- * row_merge: int32[rows] merge index of each row at this level (or -1). */
+ * Uses this level's kvf_level_stats outputs (member counts in `flag`,
+ * absorber list/count) and the pre-remap `alive` flags.
+ * row_merge: int32[rows] merge index of each row at this level (or -1).
+ * workspace: int32[kvf_merge_workspace_ints(U*NB)]. */
+int64_t kvf_merge_workspace_ints(int64_t n_total);
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L,
                      int64_t NB, int t, int h, int d, int head_mode, void* knorm,
                      void* vnorm, const void* orig_knorm, const void* orig_vnorm,
-                     const int32_t* absorber, const int32_t* merges,
-                     const int32_t* row_merge, int bpr, const int32_t* list,
-                     const int32_t* count_dev, int64_t list_cap, void* stream);
+                     const int32_t* absorber, const uint8_t* alive,
+                     const int32_t* merges, const int32_t* row_merge, int bpr,
+                     const int32_t* list, const int32_t* count_dev,
+                     const int32_t* flag, int32_t* workspace, int64_t list_cap,
+                     void* stream);
 
 /* K5 -- block-table remap + refcounts (replaces BlockTable.redirect,
  * core.py:217-227, and alive[rid] = False, fusion.py:262-264). Clears flag. */

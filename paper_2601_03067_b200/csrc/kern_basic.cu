@@ -145,7 +145,7 @@ __global__ void level_stats_kernel(int64_t u0, int64_t NB, const uint8_t* __rest
     const int32_t a = absorber[gb + j];
     if (al && a != kNone) {
       nf += 1.0;
-      if (atomicExch(&flag[gb + a], 1) == 0) {
+      if (atomicAdd(&flag[gb + a], 1) == 0) {  // flag = member count of absorber a
         const int pos = atomicAdd(count, 1);
         list[pos] = (int32_t)(gb + a);
       }
@@ -205,12 +205,40 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t
 
 // --------------------------------------------------------------------------
 // K4: merge. Persistent grid (x = absorber list stride, y = 0:K / 1:V).
-// Members of absorber l are {j in right range of l's merge : absorber[j] == l}
-// collected in ascending j (ballot + ordered prefix), so the fp summation order
-// is fixed and the result is bitwise deterministic.
+// Member lists are bucketed per absorber (count -> segment -> scatter); each
+// CTA sorts its absorber's members ascending (rank sort in smem) so the fp
+// summation order is fixed and the result is bitwise deterministic. Groups
+// larger than the smem list fall back to an ordered scan of the right range.
 // --------------------------------------------------------------------------
+constexpr int kMaxSorted = 512;
+
+__global__ void member_seg_kernel(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                                  const int32_t* __restrict__ mcnt, int32_t* mstart,
+                                  int32_t* cursor) {
+  const int n = *count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int32_t a = list[i];
+    mstart[a] = atomicAdd(cursor, mcnt[a]);
+  }
+}
+
+__global__ void member_scatter_kernel(int64_t n, int64_t NB, const uint8_t* __restrict__ alive,
+                                      const int32_t* __restrict__ absorber,
+                                      const int32_t* __restrict__ mstart, int32_t* mfill,
+                                      int32_t* members) {
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
+       x += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t aj = absorber[x];
+    if (aj != kNone && alive[x]) {
+      const int64_t a = (x / NB) * NB + aj;
+      const int slot = atomicAdd(&mfill[a], 1);
+      members[mstart[a] + slot] = (int32_t)(x % NB);
+    }
+  }
+}
+
 template <typename T, int VEC>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, 1)
 merge_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
              typename AccOf<T>::type* __restrict__ knorm,
              typename AccOf<T>::type* __restrict__ vnorm,
@@ -218,11 +246,14 @@ merge_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
              const typename AccOf<T>::type* __restrict__ ovnorm,
              const int32_t* __restrict__ absorber, const int32_t* __restrict__ merges,
              const int32_t* __restrict__ row_merge, int bpr,
-             const int32_t* __restrict__ list, const int32_t* __restrict__ count) {
+             const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+             const int32_t* __restrict__ mcnt, const int32_t* __restrict__ mstart,
+             const int32_t* __restrict__ members_g) {
   using A = typename AccOf<T>::type;
   constexpr int MAXQ = 32 / VEC;
   __shared__ A red[32];
-  __shared__ int32_t members[512];
+  __shared__ int32_t raw[kMaxSorted];
+  __shared__ int32_t members[kMaxSorted];
   __shared__ int warp_cnt[16];
   __shared__ int nmem;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -233,13 +264,33 @@ merge_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
   const A* onorm = is_v ? ovnorm : oknorm;
   const int64_t nch = g.r() / VEC;
   const int n_items = *count;
+
+  auto accumulate = [&](A (&acc)[MAXQ][VEC], int64_t u, int n) {
+    const int64_t gb = u * g.NB;
+    for (int k = 0; k < n; ++k) {
+      const int32_t jm = members[k];
+      const A nj = norm[gb + jm];
+      const A inv = nj > A(0) ? A(1) / nj : A(0);
+      const T* xj = pool + g.base(u, jm);
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int64_t c = tid + (int64_t)q * bd;
+        if (c < nch) {
+          A v[VEC];
+          VecIO<T, VEC>::load(xj + g.off(c * VEC), v);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[q][e] += v[e] * inv;
+        }
+      }
+    }
+  };
+
   for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
     const int64_t gid = list[it];
     const int64_t u = gid / g.NB;
     const int32_t l = (int32_t)(gid % g.NB);
     const int64_t gb = u * g.NB;
-    const int m = row_merge[l / bpr];
-    const int mid = merges[3 * m + 1], re = merges[3 * m + 2];
+    const int nmemb = mcnt[gid];
     A acc[MAXQ][VEC];
     {
       const A nl = norm[gid];
@@ -258,42 +309,43 @@ merge_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
         }
       }
     }
-    for (int j0 = mid; j0 < re; j0 += bd) {
-      const int j = j0 + tid;
-      const bool match = j < re && absorber[gb + j] == l;
-      const unsigned bal = __ballot_sync(0xffffffffu, match);
-      if (lane == 0) warp_cnt[warp] = __popc(bal);
+    if (nmemb <= kMaxSorted) {
+      const int s0 = mstart[gid];
+      for (int k = tid; k < nmemb; k += bd) raw[k] = members_g[s0 + k];
       __syncthreads();
-      if (tid == 0) {
-        int run = 0;
-        for (int w = 0; w < (bd >> 5); ++w) {
-          const int cnum = warp_cnt[w];
-          warp_cnt[w] = run;
-          run += cnum;
-        }
-        nmem = run;
+      for (int k = tid; k < nmemb; k += bd) {  // rank sort (ids are distinct)
+        const int32_t v = raw[k];
+        int rank = 0;
+        for (int q = 0; q < nmemb; ++q) rank += raw[q] < v;
+        members[rank] = v;
       }
       __syncthreads();
-      if (match) members[warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = j;
+      accumulate(acc, u, nmemb);
       __syncthreads();
-      const int nm_ = nmem;
-      for (int k = 0; k < nm_; ++k) {
-        const int32_t jm = members[k];
-        const A nj = norm[gb + jm];
-        const A inv = nj > A(0) ? A(1) / nj : A(0);
-        const T* xj = pool + g.base(u, jm);
-#pragma unroll
-        for (int q = 0; q < MAXQ; ++q) {
-          const int64_t c = tid + (int64_t)q * bd;
-          if (c < nch) {
-            A v[VEC];
-            VecIO<T, VEC>::load(xj + g.off(c * VEC), v);
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[q][e] += v[e] * inv;
+    } else {
+      const int m = row_merge[l / bpr];
+      const int mid = merges[3 * m + 1], re = merges[3 * m + 2];
+      for (int j0 = mid; j0 < re; j0 += bd) {
+        const int j = j0 + tid;
+        const bool match = j < re && absorber[gb + j] == l;
+        const unsigned bal = __ballot_sync(0xffffffffu, match);
+        if (lane == 0) warp_cnt[warp] = __popc(bal);
+        __syncthreads();
+        if (tid == 0) {
+          int run = 0;
+          for (int w = 0; w < (bd >> 5); ++w) {
+            const int cnum = warp_cnt[w];
+            warp_cnt[w] = run;
+            run += cnum;
           }
+          nmem = run;
         }
+        __syncthreads();
+        if (match) members[warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = j;
+        __syncthreads();
+        accumulate(acc, u, nmem);
+        __syncthreads();
       }
-      __syncthreads();
     }
     A ss = 0;
 #pragma unroll
@@ -323,56 +375,73 @@ merge_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
   }
 }
 
+struct MergeWs {  // int32 workspace: [mfill | cursor | pad | mstart | members]
+  int32_t *mfill, *cursor, *mstart, *members;
+  MergeWs(int32_t* ws, int64_t n) : mfill(ws), cursor(ws + n), mstart(ws + n + 32), members(ws + 2 * n + 32) {}
+};
+
 template <typename T, int VEC>
 static cudaError_t merge_t(void* pk, void* pv, const Geom& g, void* kn, void* vn,
                            const void* okn, const void* ovn, const int32_t* absorber,
-                           const int32_t* merges, const int32_t* row_merge, int bpr,
-                           const int32_t* list, const int32_t* count, int64_t cap,
-                           cudaStream_t s) {
+                           const uint8_t* alive, const int32_t* merges, const int32_t* row_merge,
+                           int bpr, const int32_t* list, const int32_t* count, const int32_t* mcnt,
+                           int32_t* ws, int64_t cap, cudaStream_t s) {
   using A = typename AccOf<T>::type;
   const int64_t nch = g.r() / VEC;
   int bd = 512;
   while (bd > 64 && (int64_t)(bd / 2) * (32 / VEC) >= nch) bd /= 2;  // small vectors: small CTAs
   if (nch > (int64_t)bd * (32 / VEC)) return cudaErrorInvalidValue;
-  int64_t gx = cap < 148 * 8 ? cap : 148 * 8;
+  const int64_t n = g.units() * g.NB;
+  MergeWs w(ws, n);
+  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(int32_t) * (n + 1), s);
+  if (e != cudaSuccess) return e;
+  const int sgrid = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  member_seg_kernel<<<sgrid, 256, 0, s>>>(list, count, mcnt, w.mstart, w.cursor);
+  member_scatter_kernel<<<sgrid, 256, 0, s>>>(n, g.NB, alive, absorber, w.mstart, w.mfill,
+                                              w.members);
+  int64_t gx = cap < 148 * 4 ? cap : 148 * 4;
   if (gx < 1) gx = 1;
   dim3 grid((unsigned)gx, 2);
   merge_kernel<T, VEC><<<grid, bd, 0, s>>>((T*)pk, (T*)pv, g, (A*)kn, (A*)vn, (const A*)okn,
                                            (const A*)ovn, absorber, merges, row_merge, bpr,
-                                           list, count);
+                                           list, count, mcnt, w.mstart, w.members);
   return cudaGetLastError();
 }
 
 template <typename T>
 static cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn,
                                   const void* okn, const void* ovn, const int32_t* absorber,
-                                  const int32_t* merges, const int32_t* row_merge, int bpr,
-                                  const int32_t* list, const int32_t* count, int64_t cap,
-                                  cudaStream_t s) {
+                                  const uint8_t* alive, const int32_t* merges,
+                                  const int32_t* row_merge, int bpr, const int32_t* list,
+                                  const int32_t* count, const int32_t* mcnt, int32_t* ws,
+                                  int64_t cap, cudaStream_t s) {
   if (can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g))
-    return merge_t<T, Vec16<T>::N>(pk, pv, g, kn, vn, okn, ovn, absorber, merges, row_merge,
-                                   bpr, list, count, cap, s);
-  return merge_t<T, 1>(pk, pv, g, kn, vn, okn, ovn, absorber, merges, row_merge, bpr, list,
-                       count, cap, s);
+    return merge_t<T, Vec16<T>::N>(pk, pv, g, kn, vn, okn, ovn, absorber, alive, merges,
+                                   row_merge, bpr, list, count, mcnt, ws, cap, s);
+  return merge_t<T, 1>(pk, pv, g, kn, vn, okn, ovn, absorber, alive, merges, row_merge, bpr,
+                       list, count, mcnt, ws, cap, s);
 }
+
+int64_t merge_workspace_ints(int64_t n_total) { return 3 * n_total + 64; }
 
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
                                 const void* ovnorm, const int32_t* absorber,
-                                const int32_t* merges, const int32_t* row_merge, int bpr,
-                                const int32_t* list, const int32_t* count, int64_t cap,
-                                cudaStream_t s) {
+                                const uint8_t* alive, const int32_t* merges,
+                                const int32_t* row_merge, int bpr, const int32_t* list,
+                                const int32_t* count, const int32_t* mcnt, int32_t* ws,
+                                int64_t cap, cudaStream_t s) {
   switch (dtype) {
     case F64:
       return merge_dispatch<double>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, absorber,
-                                    merges, row_merge, bpr, list, count, cap, s);
+                                    alive, merges, row_merge, bpr, list, count, mcnt, ws, cap, s);
     case F32:
       return merge_dispatch<float>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, absorber,
-                                   merges, row_merge, bpr, list, count, cap, s);
+                                   alive, merges, row_merge, bpr, list, count, mcnt, ws, cap, s);
     default:
       return merge_dispatch<__nv_bfloat16>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm,
-                                           absorber, merges, row_merge, bpr, list, count, cap,
-                                           s);
+                                           absorber, alive, merges, row_merge, bpr, list, count,
+                                           mcnt, ws, cap, s);
   }
 }
 
@@ -649,6 +718,87 @@ cudaError_t launch_refold(const void* pool, int dtype, const Geom& g, int64_t la
       refold_kernel<<<(unsigned)g.NB, 256, 0, s>>>((const __nv_bfloat16*)pool, g, layer, table,
                                                    (const float*)scale, (float*)out);
   }
+  return cudaGetLastError();
+}
+
+}  // namespace kvf
+
+namespace kvf {
+
+// --------------------------------------------------------------------------
+// compaction helpers for the top tree levels: ascending alive list + rank,
+// and a staged copy of the alive K rows (contiguous per unit) for TMA
+// --------------------------------------------------------------------------
+__global__ void alive_rank_kernel(int64_t u0, int64_t NB, const uint8_t* __restrict__ alive,
+                                  int32_t* live, int32_t* rank, int32_t* count) {
+  __shared__ int wl[32];
+  __shared__ int base;
+  const int64_t u = u0 + blockIdx.x;
+  const int64_t gb = u * NB;
+  int32_t* rk = rank + u * (NB + 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < NB; c0 += blockDim.x) {
+    const int64_t i = c0 + threadIdx.x;
+    const bool al = i < NB && alive[gb + i];
+    const unsigned bl = __ballot_sync(0xffffffffu, al);
+    if (lane == 0) wl[warp] = __popc(bl);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int run = base;
+      for (int w = 0; w < nw; ++w) {
+        const int a = wl[w];
+        wl[w] = run;
+        run += a;
+      }
+      base = run;
+    }
+    __syncthreads();
+    const int pos = wl[warp] + __popc(bl & ((1u << lane) - 1u));
+    if (i < NB) rk[i] = pos;
+    if (al) live[gb + pos] = (int32_t)i;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rk[NB] = base;
+    count[u] = base;
+  }
+}
+
+cudaError_t launch_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive,
+                              int32_t* live, int32_t* rank, int32_t* count, cudaStream_t s) {
+  if (nU == 0) return cudaSuccess;
+  alive_rank_kernel<<<(unsigned)nU, 1024, 0, s>>>(u0, NB, alive, live, rank, count);
+  return cudaGetLastError();
+}
+
+// one warp per staged row; 16-byte vectors (bf16 x 8)
+__global__ void stage_rows_kernel(const __nv_bfloat16* __restrict__ pool, Geom g, int64_t u0,
+                                  const int32_t* __restrict__ live,
+                                  const int32_t* __restrict__ count, __nv_bfloat16* staged) {
+  const int64_t ul = blockIdx.y, u = u0 + ul;
+  const int64_t k = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (k >= count[u]) return;
+  const int32_t id = live[u * g.NB + k];
+  const __nv_bfloat16* src = pool + g.base(u, id);
+  __nv_bfloat16* dst = staged + (ul * g.NB + k) * g.r();
+  const int64_t nch = g.r() / 8;
+#pragma unroll 4
+  for (int64_t c = lane; c < nch; c += 32)
+    *reinterpret_cast<uint4*>(dst + c * 8) =
+        __ldg(reinterpret_cast<const uint4*>(src + g.off(c * 8)));
+}
+
+cudaError_t launch_stage_rows(const void* pool, int dtype, const Geom& g, int64_t u0, int64_t nU,
+                              const int32_t* live, const int32_t* count, void* staged,
+                              cudaStream_t s) {
+  if (dtype != BF16 || g.d % 8 != 0) return cudaErrorInvalidValue;
+  if (nU == 0) return cudaSuccess;
+  dim3 grid((unsigned)((g.NB + 7) / 8), (unsigned)nU);
+  stage_rows_kernel<<<grid, 256, 0, s>>>((const __nv_bfloat16*)pool, g, u0, live, count,
+                                         (__nv_bfloat16*)staged);
   return cudaGetLastError();
 }
 

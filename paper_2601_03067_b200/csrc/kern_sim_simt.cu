@@ -73,11 +73,14 @@ sim_simt_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
     colmin[c_] = kNone;
   }
 
-  A acc[4][4];
+  // two-level accumulation: KC-long partial dot products in A, summed in
+  // double across chunks (a long sequential fp32 sum over r = 16K terms would
+  // cost ~1e-5 of similarity accuracy)
+  double accd[4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = A(0);
+    for (int b = 0; b < 4; ++b) accd[a][b] = 0.0;
 
   const int64_t r = g.r();
   for (int64_t k0 = 0; k0 < r; k0 += KC) {
@@ -85,6 +88,11 @@ sim_simt_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
     load_chunk<T>(As, pool, g, u, lb + i0, ni, k0, r);
     load_chunk<T>(Bs, pool, g, u, mid + j0, nj, k0, r);
     __syncthreads();
+    A acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = A(0);
 #pragma unroll 8
     for (int kk = 0; kk < KC; ++kk) {
       A av[4], bv[4];
@@ -97,8 +105,17 @@ sim_simt_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] += av[a] * bv[b];
     }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) accd[a][b] += (double)acc[a][b];
   }
   __syncthreads();
+  A acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = (A)accd[a][b];
 
   // epilogue: scale, mask, stats, per-column first match
   double cnt = 0, s1 = 0, s2 = 0, mn = INFINITY, mx = -INFINITY;

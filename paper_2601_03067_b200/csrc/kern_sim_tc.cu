@@ -1,6 +1,431 @@
-// placeholder: replaced by the tcgen05 similarity kernel
+// K2 + K3 on the 5th-gen tensor cores (sm_100a): block-similarity GEMM with
+// the first-match selection fused into the epilogue. Replaces fusion.py:244-265
+// (sim = kdir[left] @ kdir[right].T, then the per-left-row candidate loop).
+//
+// One CTA computes a 128 (left blocks) x 256 (right blocks) similarity tile of
+// one merge of one unit, K = the block vector length r (t*h*d folded, t*d per
+// head), bf16 inputs, fp32 accumulation in TMEM:
+//   warp 0      TMA producer: 4-D tensor map over the pool (d, h, t, rows),
+//               box {64, 1, 1, 128}, 128B swizzle; A = 1 box, B = 2 boxes per
+//               64-wide k-step, 4-stage mbarrier ring (48 KB / stage)
+//   warp 1      MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16 (M128 N256
+//               K16) per k-step, tcgen05.commit frees the stage
+//   warp 2      TMEM allocator (256 columns)
+//   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> sim = acc / (|x_i||x_j|),
+//               alive/fusable masks, strict '> thr', per-column min row via
+//               redux.sync + smem atomicMin -> one global atomicMin per column;
+//               similarity moments (n, sum, sumsq, min, max) per tile.
+// Raw pool rows are fed to the MMA (no normalised copy): norms are applied in
+// the epilogue, so level-1 similarities are exact-input bf16 products.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <mutex>
 #include "kernels.h"
+
 namespace kvf {
-bool tc_supported(const SimArgs& a, const char** why) { *why = "not built"; return false; }
-cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) { return cudaErrorNotSupported; }
+
+namespace {
+constexpr int BM = kTcTileM;          // 128 left blocks
+constexpr int BN = kTcTileN;          // 256 right blocks
+constexpr int BK = 64;                // bf16 elements per k-step (128 B rows)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int TMEM_COLS = 256;
+constexpr int NTHREADS = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*meta*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// K-major, 128B-swizzled UMMA shared-memory descriptor: SBO = 1024 B (8 rows
+// x 128 B), LBO unused (1), version 1 (sm_100), layout SWIZZLE_128B (2).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t desc = 0;
+  desc |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  desc |= (uint64_t)1 << 16;
+  desc |= (uint64_t)(1024 >> 4) << 32;
+  desc |= (uint64_t)1 << 46;
+  desc |= (uint64_t)2 << 61;
+  return desc;
+}
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N, M.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+}  // namespace
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
+              const float* __restrict__ knorm, const uint8_t* __restrict__ fusable,
+              const uint8_t* __restrict__ alive, int32_t* __restrict__ absorber,
+              const int32_t* __restrict__ merges, const int32_t* __restrict__ tiles, int nt,
+              float thr, double* __restrict__ partials, double* __restrict__ samples,
+              const int64_t* __restrict__ sample_off, int64_t sample_stride,
+              const int32_t* __restrict__ live, const int32_t* __restrict__ rank,
+              int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
+              float resc_band) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint8_t* meta = smem + STAGES * STAGE_BYTES;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tmem_full = empty_bar + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* inv_j = reinterpret_cast<float*>(meta + 256);
+  int32_t* colmin = reinterpret_cast<int32_t*>(meta + 256 + 4 * BN);
+  uint8_t* ok_j = meta + 256 + 8 * BN;
+  double* red = reinterpret_cast<double*>(meta + 256 + 9 * BN);  // 4 warps x 5
+  int32_t* colid = reinterpret_cast<int32_t*>(meta + 256 + 9 * BN + 256);  // block ids
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int64_t ul = blockIdx.y, u = u0 + ul;
+  const int64_t gb = u * g.NB;
+  const int m = tiles[3 * tile], i0 = tiles[3 * tile + 1], j0 = tiles[3 * tile + 2];
+  const int lb = merges[3 * m], mid = merges[3 * m + 1], re = merges[3 * m + 2];
+  // compacted mode: rows are positions in the unit's ascending alive list and
+  // the operands come from the staged (compacted) copy of the alive K rows
+  const bool staged = live != nullptr;
+  int pl = lb, pm = mid, pr = re;
+  if (staged) {
+    const int32_t* rk = rank + u * (g.NB + 1);
+    pl = rk[lb];
+    pm = rk[mid];
+    pr = rk[re];
+  }
+  const int left_n = pm - pl, right_n = pr - pm;
+  if (i0 >= left_n || j0 >= right_n) {  // tile fully beyond the alive blocks
+    if (threadIdx.x == 0) {
+      double* pp = partials + (ul * nt + tile) * 5;
+      pp[0] = pp[1] = pp[2] = 0.0;
+      pp[3] = INFINITY;
+      pp[4] = -INFINITY;
+    }
+    return;
+  }
+  const int ni = min(BM, left_n - i0), nj = min(BN, right_n - j0);
+  const int layer = g.head_mode ? (int)(u / g.h) : (int)u;
+  const int head = g.head_mode ? (int)(u % g.h) : 0;
+  const int dpc = g.d / BK;
+  const int nk = g.head_mode ? g.t * dpc : g.t * g.h * dpc;
+  const int rowA = staged ? (int)(ul * g.NB) + pl + i0 : (int)(layer * g.NB) + lb + i0;
+  const int rowB = staged ? (int)(ul * g.NB) + pm + j0 : (int)(layer * g.NB) + mid + j0;
+  const int32_t* lv = live + gb;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (warp >= 3) {  // column metadata (160 threads cover 256 columns)
+    for (int c = threadIdx.x - 96; c < BN; c += NTHREADS - 96) {
+      const int64_t bj = gb + (c < nj ? (staged ? lv[pm + j0 + c] : mid + j0 + c) : 0);
+      const bool ok = c < nj && alive[bj] && fusable[bj];
+      colid[c] = (int32_t)(bj - gb);
+      const float nv = ok ? knorm[bj] : 0.f;
+      ok_j[c] = ok;
+      inv_j[c] = nv > 0.f ? 1.f / nv : 0.f;
+      colmin[c] = kNone;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
+      for (int ks = 0; ks < nk; ++ks) {
+        const int s = ks % STAGES;
+        const uint32_t ph = (ks / STAGES) & 1;
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        const int dc = ks % dpc;
+        const int rest = ks / dpc;
+        const int hh = g.head_mode ? head : rest % g.h;
+        const int tok = g.head_mode ? rest : rest / g.h;
+        // pool map: (d, h, t, rows); staged map: (64, r/64, 1, rows)
+        const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        uint8_t* sb = sa + A_BYTES;
+        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
+        tma_load_4d(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
+        tma_load_4d(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
+        tma_load_4d(sb + A_BYTES, &tmap, &full_bar[s], c0, c1, c2, rowB + BM);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int ks = 0; ks < nk; ++ks) {
+        const int s = ks % STAGES;
+        const uint32_t ph = (ks / STAGES) & 1;
+        mbar_wait(&full_bar[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+        const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_bf16(tmem_base, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), (ks | k) != 0);
+        umma_commit(&empty_bar[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
+    const int row = ew * 32 + lane;
+    const int32_t my_id = row < ni ? (staged ? lv[pl + i0 + row] : lb + i0 + row) : 0;
+    const int64_t bi = gb + my_id;
+    const bool ok_i = row < ni && alive[bi] && fusable[bi];
+    const float ni_v = ok_i ? knorm[bi] : 0.f;
+    const float inv_i = ni_v > 0.f ? 1.f / ni_v : 0.f;
+    float cnt = 0.f, s1 = 0.f, s2 = 0.f, mn = INFINITY, mx = -INFINITY;
+    double* samp = samples ? samples + ul * sample_stride + sample_off[m] : nullptr;
+
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + c0, v);
+      int32_t mine = kNone;
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const int col = c0 + c;
+        const bool ok = ok_i && ok_j[col];
+        const float s = __uint_as_float(v[c]) * inv_i * inv_j[col];
+        int32_t cand = kNone;
+        if (ok) {
+          cnt += 1.f;
+          s1 += s;
+          s2 += s * s;
+          mn = fminf(mn, s);
+          mx = fmaxf(mx, s);
+          // The tensor-core fp32 accumulation over r/16 steps can be off by
+          // ~1e-4 relative: pairs that close to the threshold are deferred to
+          // an exact float64 re-score (kvf_rescore) instead of decided here.
+          bool decided = true;
+          if (resc != nullptr && fabsf(s - thr) <= resc_band) {
+            const int pos = atomicAdd(resc_count, 1);
+            if (pos < resc_cap) {
+              int4 e;
+              e.x = (int)u;
+              e.y = my_id;
+              e.z = colid[col];
+              e.w = m;
+              reinterpret_cast<int4*>(resc)[pos] = e;
+              decided = false;
+            }
+          }
+          if (decided && s > thr) cand = my_id;
+        }
+        if (samp && row < ni && col < nj)
+          samp[(int64_t)(my_id - lb) * (re - mid) + (colid[col] - mid)] = ok ? (double)s : (double)NAN;
+        const int32_t wmin = (int32_t)__reduce_min_sync(0xffffffffu, (uint32_t)cand);
+        if (lane == c) mine = wmin;
+      }
+      if (mine != kNone) atomicMin(&colmin[c0 + lane], mine);
+    }
+    // per-tile similarity moments: deterministic warp tree, then fixed warp order
+    double dc = cnt, d1 = s1, d2 = s2, dmn = mn, dmx = mx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dc += __shfl_xor_sync(0xffffffffu, dc, o);
+      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+      d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+    }
+    if (lane == 0) {
+      red[ew * 5 + 0] = dc;
+      red[ew * 5 + 1] = d1;
+      red[ew * 5 + 2] = d2;
+      red[ew * 5 + 3] = dmn;
+      red[ew * 5 + 4] = dmx;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    for (int c = threadIdx.x - 128; c < BN; c += 128) {
+      const int32_t cm = colmin[c];
+      if (cm != kNone) atomicMin(&absorber[gb + colid[c]], cm);
+    }
+    if (threadIdx.x == 128) {
+      double o[5] = {0, 0, 0, INFINITY, -INFINITY};
+      for (int w = 0; w < 4; ++w) {
+        o[0] += red[w * 5 + 0];
+        o[1] += red[w * 5 + 1];
+        o[2] += red[w * 5 + 2];
+        o[3] = fmin(o[3], red[w * 5 + 3]);
+        o[4] = fmax(o[4], red[w * 5 + 4]);
+      }
+      double* pp = partials + (ul * nt + tile) * 5;
+      for (int q = 0; q < 5; ++q) pp[q] = o[q];
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+}  // namespace
+
+bool tc_supported(const SimArgs& a, const char** why) {
+  if (a.dtype != BF16) {
+    *why = "pool dtype is not bfloat16";
+    return false;
+  }
+  if (a.g.d % BK != 0) {
+    *why = "head dim must be a multiple of 64";
+    return false;
+  }
+  if ((reinterpret_cast<uintptr_t>(a.pool) & 15) != 0) {
+    *why = "pool pointer must be 16-byte aligned";
+    return false;
+  }
+  if (a.g.L * a.g.NB >= (int64_t)INT32_MAX - 512) {
+    *why = "too many pool rows for int32 TMA coordinates";
+    return false;
+  }
+  int dev = 0, major = 0, minor = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0) {
+    *why = "tcgen05 kernels are built for sm_100a (B200)";
+    return false;
+  }
+  if (!get_encode()) {
+    *why = "cuTensorMapEncodeTiled unavailable";
+    return false;
+  }
+  return true;
+}
+
+cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
+  if (a.nt == 0 || a.nU == 0) return cudaSuccess;
+  CUtensorMap tmap;
+  const Geom& g = a.g;
+  const bool staged = a.live != nullptr;
+  const cuuint64_t r = (cuuint64_t)g.r();
+  cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.h, (cuuint64_t)g.t,
+                        (cuuint64_t)(g.L * g.NB)};
+  cuuint64_t strides[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.h * g.d * 2,
+                           (cuuint64_t)g.t * g.h * g.d * 2};
+  if (staged) {  // staged rows: [nU * NB][r] -> (64, r/64, 1, rows)
+    dims[0] = BK;
+    dims[1] = r / BK;
+    dims[2] = 1;
+    dims[3] = (cuuint64_t)(a.nU * g.NB);
+    strides[0] = BK * 2;
+    strides[1] = r * 2;
+    strides[2] = r * 2;
+  }
+  cuuint32_t box[4] = {(cuuint32_t)BK, 1, 1, (cuuint32_t)BM};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult res = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                            const_cast<void*>(staged ? a.staged : a.pool),
+                            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(sim_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  float thr = (float)a.thr;
+  if ((double)thr > a.thr) thr = nextafterf(thr, -INFINITY);  // (float)s > thr_f <=> s > thr
+  dim3 grid(a.nt, (unsigned)a.nU);
+  sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(tmap, g, a.u0, (const float*)a.knorm, a.fusable,
+                                                   a.alive, a.absorber, a.merges, a.tiles, a.nt,
+                                                   thr, a.partials, a.samples, a.sample_off,
+                                                   a.sample_stride, a.live, a.rank, a.resc,
+                                                   a.resc_count, (int)a.resc_cap,
+                                                   (float)a.resc_band);
+  return cudaGetLastError();
+}
+
+}  // namespace kvf

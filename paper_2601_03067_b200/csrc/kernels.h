@@ -33,7 +33,34 @@ struct SimArgs {
   double* samples;
   const int64_t* sample_off;
   int64_t sample_stride;
+  // compaction (tcgen05 path): ascending alive ids / exclusive alive rank
+  // [U][NB + 1] / staged K rows [nU][NB][r] (bf16); all null = direct mode
+  const int32_t* live = nullptr;
+  const int32_t* rank = nullptr;
+  const void* staged = nullptr;
+  // near-threshold re-score queue (tcgen05 path): int4 {u, i, j, merge}
+  int32_t* resc = nullptr;
+  int32_t* resc_count = nullptr;
+  int64_t resc_cap = 0;
+  double resc_band = 0.0;
 };
+
+struct RescoreArgs {
+  const void* pool;
+  int dtype;
+  Geom g;
+  int64_t u0;
+  const int32_t* resc;
+  const int32_t* resc_count;
+  int64_t resc_cap;
+  double thr;
+  int32_t* absorber;
+  const int32_t* merges;
+  double* samples;
+  const int64_t* sample_off;
+  int64_t sample_stride;
+};
+cudaError_t launch_rescore(const RescoreArgs& a, cudaStream_t s);
 
 constexpr int kSimtTile = 64;
 cudaError_t launch_sim_simt(const SimArgs& a, cudaStream_t s);
@@ -49,12 +76,19 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t
                                const int32_t* merges, int nm, const int32_t* tile_off,
                                int nt, const double* partials, double* stats,
                                int32_t* flag, int32_t* list, int32_t* count, cudaStream_t s);
+int64_t merge_workspace_ints(int64_t n_total);
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
                                 const void* ovnorm, const int32_t* absorber,
-                                const int32_t* merges, const int32_t* row_merge, int bpr,
-                                const int32_t* list, const int32_t* count, int64_t cap,
-                                cudaStream_t s);
+                                const uint8_t* alive, const int32_t* merges,
+                                const int32_t* row_merge, int bpr, const int32_t* list,
+                                const int32_t* count, const int32_t* mcnt, int32_t* ws,
+                                int64_t cap, cudaStream_t s);
+cudaError_t launch_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive,
+                              int32_t* live, int32_t* rank, int32_t* count, cudaStream_t s);
+cudaError_t launch_stage_rows(const void* pool, int dtype, const Geom& g, int64_t u0, int64_t nU,
+                              const int32_t* live, const int32_t* count, void* staged,
+                              cudaStream_t s);
 cudaError_t launch_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber,
                          int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* flag,
                          cudaStream_t s);

@@ -104,8 +104,10 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
                           const uint8_t* fusable, const uint8_t* alive, int32_t* absorber,
                           const int32_t* merges, int nm, const int32_t* tiles, int nt,
                           double thr, double* partials, double* samples,
-                          const int64_t* sample_off, int64_t sample_stride, int path,
-                          void* stream) {
+                          const int64_t* sample_off, int64_t sample_stride,
+                          const int32_t* live, const int32_t* rank, const void* staged,
+                          int32_t* rescore_queue, int64_t rescore_cap, double rescore_band,
+                          int path, void* stream) {
   SimArgs a;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
   if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
@@ -135,12 +137,34 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
   a.samples = samples;
   a.sample_off = sample_off;
   a.sample_stride = sample_stride;
+  a.live = live;
+  a.rank = rank;
+  a.staged = staged;
+  if ((live != nullptr) != (rank != nullptr) || (live != nullptr) != (staged != nullptr))
+    return fail(KVF_ERR_INVALID, "compaction needs live, rank and staged together");
   if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
+  if (live && path != KVF_PATH_TC)
+    return fail(KVF_ERR_INVALID, "compacted similarity requires the tcgen05 path");
   if (path == KVF_PATH_TC) {
     const char* why = "";
     if (!tc_supported(a, &why))
       return fail(KVF_ERR_INVALID, "tcgen05 similarity path unavailable: %s", why);
-    return cuda_status(launch_sim_tc(a, (cudaStream_t)stream), "kvf_similarity_select[tc]");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool resc = rescore_queue != nullptr && rescore_cap > 0 && rescore_band > 0.0;
+    if (resc) {
+      if (rescore_cap > INT32_MAX / 4) return fail(KVF_ERR_INVALID, "rescore queue too large");
+      a.resc = rescore_queue;
+      a.resc_count = rescore_queue + 4 * rescore_cap;
+      a.resc_cap = rescore_cap;
+      a.resc_band = rescore_band;
+      cudaError_t e = cudaMemsetAsync(a.resc_count, 0, sizeof(int32_t), st);
+      if (e != cudaSuccess) return cuda_status(e, "kvf_similarity_select[tc]");
+    }
+    if (int rc = cuda_status(launch_sim_tc(a, st), "kvf_similarity_select[tc]")) return rc;
+    if (!resc) return KVF_OK;
+    RescoreArgs r{pool_k, dtype, a.g, u0, a.resc, a.resc_count, rescore_cap, thr, absorber,
+                  merges, samples, sample_off, sample_stride};
+    return cuda_status(launch_rescore(r, st), "kvf_similarity_select[rescore]");
   }
   if (path != KVF_PATH_SIMT) return fail(KVF_ERR_INVALID, "unknown path %d", path);
   return cuda_status(launch_sim_simt(a, (cudaStream_t)stream), "kvf_similarity_select[simt]");
@@ -159,24 +183,49 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
                      "kvf_level_stats");
 }
 
+int64_t kvf_merge_workspace_ints(int64_t n_total) { return merge_workspace_ints(n_total); }
+
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t NB, int t, int h,
                      int d, int head_mode, void* knorm, void* vnorm, const void* orig_knorm,
-                     const void* orig_vnorm, const int32_t* absorber, const int32_t* merges,
-                     const int32_t* row_merge, int bpr, const int32_t* list,
-                     const int32_t* count_dev, int64_t list_cap, void* stream) {
+                     const void* orig_vnorm, const int32_t* absorber, const uint8_t* alive,
+                     const int32_t* merges, const int32_t* row_merge, int bpr,
+                     const int32_t* list, const int32_t* count_dev, const int32_t* flag,
+                     int32_t* workspace, int64_t list_cap, void* stream) {
   Geom g;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
   if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
   if (bpr < 1) return fail(KVF_ERR_INVALID, "bpr must be >= 1");
+  if (!pool_k || !pool_v || !knorm || !vnorm || !absorber || !alive || !list || !count_dev ||
+      !flag || !workspace)
+    return fail(KVF_ERR_INVALID, "null pointer");
   const int64_t r = g.r();
-  const int64_t rmax = dtype == F64 ? 16384 : 32768;
-  if (r > rmax)
-    return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's %lld",
-                (long long)r, (long long)rmax);
+  if (r > 16384)
+    return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's 16384",
+                (long long)r);
   cudaError_t e = launch_merge_groups(pool_k, pool_v, dtype, g, knorm, vnorm, orig_knorm,
-                                      orig_vnorm, absorber, merges, row_merge, bpr, list,
-                                      count_dev, list_cap, (cudaStream_t)stream);
+                                      orig_vnorm, absorber, alive, merges, row_merge, bpr, list,
+                                      count_dev, flag, workspace, list_cap, (cudaStream_t)stream);
   return cuda_status(e, "kvf_merge_groups");
+}
+
+int kvf_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive, int32_t* live,
+                   int32_t* rank, int32_t* count, void* stream) {
+  if (!alive || !live || !rank || !count) return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_alive_rank(u0, nU, NB, alive, live, rank, count, (cudaStream_t)stream),
+                     "kvf_alive_rank");
+}
+
+int kvf_stage_rows(const void* pool, int dtype, int64_t L, int64_t NB, int t, int h, int d,
+                   int head_mode, int64_t u0, int64_t nU, const int32_t* live,
+                   const int32_t* count, void* staged, void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (dtype != BF16 || d % 8 != 0)
+    return fail(KVF_ERR_INVALID, "row staging needs a bf16 pool with d %% 8 == 0");
+  if (u0 < 0 || nU < 0 || u0 + nU > g.units()) return fail(KVF_ERR_INVALID, "bad unit range");
+  return cuda_status(
+      launch_stage_rows(pool, dtype, g, u0, nU, live, count, staged, (cudaStream_t)stream),
+      "kvf_stage_rows");
 }
 
 int kvf_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber, int32_t* table,

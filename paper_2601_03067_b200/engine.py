@@ -26,6 +26,9 @@ from .errors import ConfigError
 from .schedule import Plan
 
 NONE = 0x7FFFFFFF
+# tcgen05 path: pairs with |sim - thr| <= RESCORE_BAND are re-decided in float64
+RESCORE_BAND = 2.0**-11
+RESCORE_CAP = 1 << 20
 
 _DT = {torch.float64: N.DT_F64, torch.float32: N.DT_F32, torch.bfloat16: N.DT_BF16}
 
@@ -150,7 +153,8 @@ class FusionState:
 class FusionEngine:
     """Runs fusion of all units of a geometry for one plan (see module doc)."""
 
-    def __init__(self, geom: Geometry, plan: Plan, dtype: torch.dtype, device, path: int = N.PATH_AUTO):
+    def __init__(self, geom: Geometry, plan: Plan, dtype: torch.dtype, device, path: int = N.PATH_AUTO,
+                 compact_from: int | None | str = "auto"):
         if plan.n_blocks != geom.NB:
             raise ConfigError(f"plan covers {plan.n_blocks} blocks, geometry has {geom.NB}")
         self.geom = geom
@@ -169,6 +173,26 @@ class FusionEngine:
         self.flag = torch.zeros(U * NB, dtype=torch.int32, device=dev)
         self.list = torch.empty(U * NB, dtype=torch.int32, device=dev)
         self.count = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.merge_ws = torch.empty(int(N.lib().kvf_merge_workspace_ints(U * NB)), dtype=torch.int32,
+                                    device=dev)
+        # compaction of the top levels (tcgen05 path): dead blocks dominate the
+        # upper merges' rectangles, so their alive K rows are staged densely
+        if compact_from == "auto":
+            compact_from = plan.tree_depth - 1 if plan.tree_depth >= 4 else None
+        if path != N.PATH_TC or geom.d % 8 != 0:
+            compact_from = None
+        self.compact_from = compact_from
+        # exact float64 re-score of pairs within RESCORE_BAND of the threshold
+        # (tensor-core fp32 accumulation error is ~1e-4 relative at r = 16K)
+        self.rescore_cap = RESCORE_CAP if path == N.PATH_TC else 0
+        self.rescore = (torch.empty(4 * (self.rescore_cap + 1), dtype=torch.int32, device=dev)
+                        if self.rescore_cap else None)
+        self.staged = None
+        if compact_from is not None:
+            self.live = torch.empty((U, NB), dtype=torch.int32, device=dev)
+            self.rank = torch.empty((U, NB + 1), dtype=torch.int32, device=dev)
+            self.acount = torch.empty(U, dtype=torch.int32, device=dev)
+            self.staged = torch.empty(U * NB * geom.r, dtype=torch.bfloat16, device=dev)
 
     def run(
         self,
@@ -225,6 +249,14 @@ class FusionEngine:
             samples = None
             if keep_samples:
                 samples = torch.empty((U, max(lv["rect_total"], 1)), dtype=torch.float64, device=dev)
+                samples.view(torch.int64).fill_(-1)  # all-ones bit pattern = NaN
+            compact = self.compact_from is not None and self.plan.levels[li].height >= self.compact_from
+            if compact:
+                N.call("kvf_alive_rank", 0, U, NB, N.ptr(alive_t), N.ptr(self.live), N.ptr(self.rank),
+                       N.ptr(self.acount), sp)
+                N.call("kvf_stage_rows", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(self.live),
+                       N.ptr(self.acount), N.ptr(self.staged), sp)
+                launches += 2
             if time_sim:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -234,8 +266,13 @@ class FusionEngine:
                 N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber), N.ptr(lv["merges"]), nm,
                 N.ptr(lv["tiles"]), nt, float(threshold), N.ptr(self.partials), N.ptr(samples),
                 N.ptr(lv["sample_off"]) if samples is not None else None,
-                samples.shape[1] if samples is not None else 0, self.path, sp,
+                samples.shape[1] if samples is not None else 0,
+                N.ptr(self.live) if compact else None, N.ptr(self.rank) if compact else None,
+                N.ptr(self.staged) if compact else None, N.ptr(self.rescore), self.rescore_cap,
+                RESCORE_BAND if self.rescore_cap else 0.0, self.path, sp,
             )
+            if self.rescore_cap:
+                launches += 1
             if time_sim:
                 e1.record(stream)
                 st.sim_events.append((e0, e1, li))
@@ -247,15 +284,15 @@ class FusionEngine:
             )
             N.call(
                 "kvf_merge_groups", N.ptr(pool_k), N.ptr(pool_v), dt, *g.args(), N.ptr(knorm),
-                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(absorber), N.ptr(lv["merges"]),
-                N.ptr(lv["row_merge"]), self.plan.bpr, N.ptr(self.list), N.ptr(self.count),
-                U * NB, sp,
+                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(absorber), N.ptr(alive_t),
+                N.ptr(lv["merges"]), N.ptr(lv["row_merge"]), self.plan.bpr, N.ptr(self.list),
+                N.ptr(self.count), N.ptr(self.flag), N.ptr(self.merge_ws), U * NB, sp,
             )
             N.call(
                 "kvf_remap", 0, U, NB, N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t),
                 N.ptr(alive_t), N.ptr(self.flag), sp,
             )
-            launches += 4
+            launches += 6
             st.level_stats.append(stats)
             st.level_samples.append(samples)
         st.k_scale = torch.empty((U, NB), dtype=acc, device=dev)
@@ -289,7 +326,7 @@ def _tc_geometry_ok(geom: Geometry) -> bool:
     return geom.d % 64 == 0 and _TC_ENABLED
 
 
-_TC_ENABLED = False
+_TC_ENABLED = True
 
 
 def audit(table: torch.Tensor, refcount: torch.Tensor, alive: torch.Tensor, U: int, NB: int) -> bool:

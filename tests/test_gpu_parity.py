@@ -18,7 +18,13 @@ K = pytest.importorskip("paper_2601_03067_b200")
 from paper_2601_03067_b200.workload import synthetic_kv  # noqa: E402
 
 # epsilon of the near-threshold exemption and direction tolerances per dtype
-EPS = {torch.float32: 2e-5, torch.bfloat16: 2e-3}
+EPS = {torch.float32: 2e-5, torch.bfloat16: 1e-3}
+# reported similarity samples: bf16 tiles carry the tensor-core fp32
+# accumulation error (~1e-4 relative at r = 16K); decisions near the
+# threshold are re-scored exactly, so for bf16 EPS covers the bf16 storage of
+# fused directions at levels >= 2 (up to ~2.5e-4 observed at r = 2048; it
+# shrinks ~1/sqrt(r)), with the usual 4x margin
+SAMPLE_TOL = {torch.float32: 5e-6, torch.bfloat16: 5e-4}
 DIR_TOL = {torch.float32: 2e-6, torch.bfloat16: 2.0**-8}
 # bf16 directions are re-rounded at every level they are rewritten
 DIR_RTOL = {torch.float32: 0.0, torch.bfloat16: 2.0**-7}
@@ -49,7 +55,7 @@ def _compare_unit(oc, ref: O.OracleResult, dtype, keep_samples=True):
         want = ref.samples()
         assert got.shape == want.shape
         err = float(np.abs(got - want).max()) if got.size else 0.0
-        assert err <= EPS[dtype] / 4, f"max |sim_gpu - sim_ref| = {err:.3g} exceeds eps/4"
+        assert err <= SAMPLE_TOL[dtype], f"max |sim_gpu - sim_ref| = {err:.3g}"
         return err
     return 0.0
 
