@@ -68,9 +68,10 @@ int kvf_state_init(int dtype, int64_t U, int64_t NB, const void* knorm,
                    int32_t* table, int32_t* refcount, void* stream);
 
 /* Similarity tile shape used by a path (tiles passed to
- * kvf_similarity_select must be built with it). */
+ * kvf_similarity_select must be built with it) and the number of partials
+ * slots each tile writes (the tcgen05 path runs one tile per CTA pair). */
 int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
-                       int* tile_n);
+                       int* tile_n, int* partials_per_tile);
 
 /* K2 + K3 -- similarity + first-match selection for every merge of one tree
  * level (replaces fusion.py:244-265):
@@ -78,7 +79,8 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
  *   absorber[j] = min { i in left : sim(i, j) > thr }   (atomicMin).
  * merges : int32[nm][3] block ranges {left_begin, split, right_end};
  * tiles  : int32[nt][3] {merge, i0, j0} offsets inside the merge;
- * partials (out): double[nU][nt][5] = {count, sum, sumsq, min, max} of sim;
+ * partials (out): double[nU][nt * partials_per_tile][5] = {count, sum,
+ *   sumsq, min, max} of sim (kvf_level_stats takes the same scaled counts);
  * samples (optional, out): double, samples[(u-u0)*sample_stride +
  *   sample_off[m] + il*right_n + jl] = sim or NaN for masked pairs (compacted
  *   launches leave dead pairs untouched: pre-fill with NaN).

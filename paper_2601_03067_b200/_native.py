@@ -38,7 +38,9 @@ SIGNATURES: dict[str, tuple] = {
     "kvf_count_nonfinite": (_i32, [_vp, _i32, _i64, _vp, _vp]),
     "kvf_block_norms": (_i32, [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),
     "kvf_state_init": (_i32, [_i32, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
-    "kvf_sim_tile_shape": (_i32, [_i32, _i32, _i32, C.POINTER(_i32), C.POINTER(_i32)]),
+    "kvf_sim_tile_shape": (
+        _i32, [_i32, _i32, _i32, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]
+    ),
     "kvf_similarity_select": (
         _i32,
         [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp,

@@ -7,6 +7,7 @@
 // Split-K (flash-decoding): CTA = (request, kv head, split of CB blocks),
 // online softmax per query head of the GQA group, then a combine kernel.
 #include "kernels.h"
+#include <type_traits>
 #include "vec_io.cuh"
 
 namespace kvf {
@@ -178,9 +179,220 @@ __global__ void decode_combine_kernel(const A* __restrict__ part, int64_t nsplit
   }
 }
 
+// ---------------------------------------------------------------------------
+// Bandwidth path (bf16 / f32 pools, d in {64, 128}): CTA = (split of CB
+// blocks, kv head, request) with one warp per query head of the GQA group.
+// 32-token K/V tiles are gathered through the block table with cp.async
+// (16-byte chunks, 3-stage ring, padded rows -> conflict-free smem), so every
+// K/V byte is read from HBM once per (request, kv head) and shared by the
+// group's warps. QK: lane = token, q broadcast from smem; PV: lane = 4 dims.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int TOK = 32;
+constexpr int STG = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+}  // namespace
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256)
+decode_fast_kernel(const void* __restrict__ q, int q_dtype, const T* __restrict__ pool_k,
+                   const T* __restrict__ pool_v, Geom g, int64_t layer,
+                   const int32_t* __restrict__ table, const float* __restrict__ k_scale,
+                   const float* __restrict__ v_scale, int64_t p_blocks,
+                   const int32_t* __restrict__ seq_blocks, int Hq, float sm_scale,
+                   float* __restrict__ part, float* __restrict__ probs) {
+  constexpr int ROW = D * (int)sizeof(T) + 16;   // padded row bytes
+  constexpr int CPR = D * (int)sizeof(T) / 16;   // 16-byte chunks per row
+  constexpr int DPL = D / 32;                    // output dims per lane
+  extern __shared__ __align__(16) uint8_t dsm[];
+  uint8_t* kt = dsm;                              // [STG][TOK][ROW]
+  uint8_t* vt = kt + STG * TOK * ROW;             // [STG][TOK][ROW]
+  float* qs = reinterpret_cast<float*>(vt + STG * TOK * ROW);  // [G][D]
+  float* sk = qs + 8 * D;                         // [STG][TOK]
+  float* sv = sk + STG * TOK;                     // [STG][TOK]
+
+  const int G = Hq / g.h;
+  const int nthr = 32 * G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = blockIdx.z;
+  const int kvh = blockIdx.y;
+  const int64_t split = blockIdx.x, nsplit = gridDim.x;
+  const int64_t unit = g.head_mode ? layer * g.h + kvh : layer;
+  const int32_t* tab = table + unit * g.NB;
+  const float* ksc = k_scale + unit * g.NB;
+  const float* vsc = v_scale + unit * g.NB;
+  const int64_t nblk = seq_blocks ? (int64_t)seq_blocks[b] : p_blocks;
+  const int64_t ntok = nblk * g.t;
+  const int64_t T0 = split * (int64_t)CB * g.t;
+  const int64_t T1 = min(T0 + (int64_t)CB * g.t, ntok);
+  const int ntiles = T1 > T0 ? (int)((T1 - T0 + TOK - 1) / TOK) : 0;
+  const int64_t E = g.E();
+  const int64_t rstride = (int64_t)g.h * D;  // token stride inside a block
+
+  for (int x = threadIdx.x; x < G * D; x += nthr) {
+    const int gg = x / D, e = x % D;
+    const int64_t qi = (b * Hq + (int64_t)kvh * G + gg) * D + e;
+    qs[gg * D + e] = q_dtype == BF16 ? __bfloat162float(((const __nv_bfloat16*)q)[qi])
+                                     : ((const float*)q)[qi];
+  }
+
+  auto issue = [&](int it) {
+    const int st = it % STG;
+    const int64_t tok0 = T0 + (int64_t)it * TOK;
+    for (int c = threadIdx.x; c < TOK * CPR; c += nthr) {
+      const int row = c / CPR, col = c % CPR;
+      const int64_t tok = tok0 + row;
+      const bool valid = tok < T1;
+      const int64_t tk = valid ? tok : T0;
+      const int64_t slot = b * p_blocks + tk / g.t;
+      const int64_t off = (layer * g.NB + tab[slot]) * E + (tk % g.t) * rstride + (int64_t)kvh * D;
+      cp_async16(kt + (st * TOK + row) * ROW + col * 16,
+                 reinterpret_cast<const uint8_t*>(pool_k + off) + col * 16, valid);
+      cp_async16(vt + (st * TOK + row) * ROW + col * 16,
+                 reinterpret_cast<const uint8_t*>(pool_v + off) + col * 16, valid);
+    }
+    for (int row = threadIdx.x; row < TOK; row += nthr) {
+      const int64_t tok = tok0 + row;
+      const bool valid = tok < T1;
+      const int64_t slot = b * p_blocks + (valid ? tok : T0) / g.t;
+      sk[st * TOK + row] = valid ? ksc[slot] : 0.f;
+      sv[st * TOK + row] = valid ? vsc[slot] : 0.f;
+    }
+    cp_commit();
+  };
+
+  float m_run = -INFINITY, l_run = 0.f;
+  float o[DPL];
+#pragma unroll
+  for (int k = 0; k < DPL; ++k) o[k] = 0.f;
+  const float* qg = qs + warp * D;
+
+  for (int it = 0; it < STG - 1; ++it) {
+    if (it < ntiles) issue(it);
+    else cp_commit();
+  }
+  for (int it = 0; it < ntiles; ++it) {
+    if (it + STG - 1 < ntiles) issue(it + STG - 1);
+    else cp_commit();
+    cp_wait<STG - 1>();
+    __syncthreads();
+    const int st = it % STG;
+    const int64_t tok = T0 + (int64_t)it * TOK + lane;
+    const bool valid = tok < T1;
+    // ---- logits: lane = token ----
+    const uint8_t* krow = kt + (st * TOK + lane) * ROW;
+    float dot = 0.f;
+#pragma unroll
+    for (int c = 0; c < CPR; ++c) {
+      constexpr int EPC = 16 / (int)sizeof(T);
+      float kv[EPC];
+      if constexpr (sizeof(T) == 2) {
+        VecIO<__nv_bfloat16, 8>::unpack(*reinterpret_cast<const uint4*>(krow + c * 16), kv);
+      } else {
+        const float4 f = *reinterpret_cast<const float4*>(krow + c * 16);
+        kv[0] = f.x; kv[1] = f.y; kv[2] = f.z; kv[3] = f.w;
+      }
+#pragma unroll
+      for (int e = 0; e < EPC; ++e) dot = fmaf(kv[e], qg[c * EPC + e], dot);
+    }
+    const float logit = valid ? dot * sk[st * TOK + lane] * sm_scale : -INFINITY;
+    if (probs && valid)
+      probs[(b * Hq + (int64_t)kvh * G + warp) * p_blocks * g.t + tok] = logit;
+    float mx = logit;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    const float m_new = fmaxf(m_run, mx);
+    const float alpha = m_new == -INFINITY ? 1.f : __expf(m_run - m_new);
+    const float pr = valid ? __expf(logit - m_new) : 0.f;
+    float ps = pr;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, s);
+    l_run = l_run * alpha + ps;
+    m_run = m_new;
+    // ---- PV: lane = DPL output dims ----
+    const float pv = pr * sv[st * TOK + lane];
+#pragma unroll
+    for (int k = 0; k < DPL; ++k) o[k] *= alpha;
+#pragma unroll 8
+    for (int tk = 0; tk < TOK; ++tk) {
+      const float w = __shfl_sync(0xffffffffu, pv, tk);
+      const uint8_t* vrow = vt + (st * TOK + tk) * ROW + lane * DPL * (int)sizeof(T);
+      float vv[DPL];
+      if constexpr (sizeof(T) == 2) {
+        if constexpr (DPL == 4) {
+          const uint2 u = *reinterpret_cast<const uint2*>(vrow);
+          const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+          const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+          vv[0] = f0.x; vv[1] = f0.y; vv[2] = f1.x; vv[3] = f1.y;
+        } else {
+          const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(vrow));
+          vv[0] = f0.x; vv[1] = f0.y;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < DPL; ++k) vv[k] = reinterpret_cast<const float*>(vrow)[k];
+      }
+#pragma unroll
+      for (int k = 0; k < DPL; ++k) o[k] = fmaf(w, vv[k], o[k]);
+    }
+    __syncthreads();
+  }
+  cp_wait<0>();
+  float* pp = part + (((b * Hq + (int64_t)kvh * G + warp) * nsplit) + split) * (D + 2);
+#pragma unroll
+  for (int k = 0; k < DPL; ++k) pp[lane * DPL + k] = o[k];
+  if (lane == 0) {
+    pp[D] = m_run;
+    pp[D + 1] = l_run;
+  }
+}
+
+template <typename T, int D>
+static cudaError_t decode_fast_t(const DecodeArgs& a, cudaStream_t s) {
+  const int G = a.Hq / a.g.h;
+  const int64_t nsplit = nsplit_of(a.p_blocks);
+  const int smem = 2 * STG * TOK * (D * (int)sizeof(T) + 16) + 8 * D * 4 + 2 * STG * TOK * 4;
+  static bool attr_set = false;  // one per <T, D> instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(decode_fast_kernel<T, D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grid((unsigned)nsplit, a.g.h, (unsigned)a.B);
+  decode_fast_kernel<T, D><<<grid, 32 * G, smem, s>>>(
+      a.q, a.q_dtype, (const T*)a.pool_k, (const T*)a.pool_v, a.g, a.layer, a.table,
+      (const float*)a.k_scale, (const float*)a.v_scale, a.p_blocks, a.seq_blocks, a.Hq,
+      (float)a.sm_scale, (float*)a.ws, (float*)a.probs);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  decode_combine_kernel<float><<<(unsigned)(a.B * a.Hq), 128, 0, s>>>(
+      (const float*)a.ws, nsplit, a.g.d, a.p_blocks, a.g.t, a.seq_blocks, a.Hq, (float*)a.out,
+      (float*)a.lse, (float*)a.probs);
+  return cudaGetLastError();
+}
+
 template <typename T>
 static cudaError_t decode_t(const DecodeArgs& a, cudaStream_t s) {
   using A = typename AccOf<T>::type;
+  if constexpr (!std::is_same<T, double>::value) {
+    const bool qok = a.q_dtype == BF16 || a.q_dtype == F32;
+    if (qok && (a.g.d == 128 || a.g.d == 64)) {
+      if (a.g.d == 128) return decode_fast_t<T, 128>(a, s);
+      return decode_fast_t<T, 64>(a, s);
+    }
+  }
   const int64_t nsplit = nsplit_of(a.p_blocks);
   dim3 grid((unsigned)nsplit, a.g.h, (unsigned)a.B);
   decode_partial_kernel<T><<<grid, NTD, 0, s>>>(

@@ -2,19 +2,24 @@
 // the first-match selection fused into the epilogue. Replaces fusion.py:244-265
 // (sim = kdir[left] @ kdir[right].T, then the per-left-row candidate loop).
 //
-// One CTA computes a 128 (left blocks) x 256 (right blocks) similarity tile of
-// one merge of one unit, K = the block vector length r (t*h*d folded, t*d per
-// head), bf16 inputs, fp32 accumulation in TMEM:
-//   warp 0      TMA producer: 4-D tensor map over the pool (d, h, t, rows),
-//               box {64, 1, 1, 128}, 128B swizzle; A = 1 box, B = 2 boxes per
-//               64-wide k-step, 4-stage mbarrier ring (48 KB / stage)
-//   warp 1      MMA issuer: 4 x tcgen05.mma.cta_group::1.kind::f16 (M128 N256
-//               K16) per k-step, tcgen05.commit frees the stage
-//   warp 2      TMEM allocator (256 columns)
-//   warps 4..7  epilogue: tcgen05.ld 32x32b.x32 -> sim = acc / (|x_i||x_j|),
-//               alive/fusable masks, strict '> thr', per-column min row via
-//               redux.sync + smem atomicMin -> one global atomicMin per column;
-//               similarity moments (n, sum, sumsq, min, max) per tile.
+// A CTA pair (cluster of 2, tcgen05 cta_group::2) computes a 256 (left
+// blocks) x 256 (right blocks) similarity tile of one merge of one unit,
+// K = the block vector length r (t*h*d folded, t*d per head), bf16 inputs,
+// fp32 accumulation in TMEM. Each CTA stages its 128 A rows and its 128-row
+// half of B; the leader issues M256 N256 K16 MMAs over both CTAs' smem:
+//   warp 0      TMA producer (both CTAs): 4-D tensor map over the pool
+//               (d, h, t, rows) or over the staged alive rows, box
+//               {64, 1, 1, 128}, 128B swizzle, 6-stage ring of 32 KB; both
+//               CTAs' bytes complete on the leader's full barrier
+//   warp 1      MMA issuer (leader): 4 x tcgen05.mma.cta_group::2.kind::f16
+//               per 64-wide k-step; tcgen05.commit multicasts the stage
+//               release to both CTAs
+//   warp 2      TMEM allocator (256 columns, cta_group::2)
+//   warps 3-7   column metadata; warps 4..7 epilogue: tcgen05.ld 32x32b.x32
+//               -> sim = acc / (|x_i||x_j|), alive/fusable masks, strict
+//               '> thr' (pairs within resc_band deferred to the exact
+//               re-score), per-column min row via redux.sync + smem atomicMin
+//               -> one global atomicMin per column; similarity moments per CTA.
 // Raw pool rows are fed to the MMA (no normalised copy): norms are applied in
 // the epilogue, so level-1 similarities are exact-input bf16 products.
 #include <cuda.h>
@@ -25,19 +30,30 @@
 namespace kvf {
 
 namespace {
-constexpr int BM = kTcTileM;          // 128 left blocks
-constexpr int BN = kTcTileN;          // 256 right blocks
+constexpr int BM = 128;               // A rows per CTA (M = 256 per pair)
+constexpr int BN = kTcTileN;          // 256 right blocks per pair (N)
+constexpr int BNH = BN / 2;           // B rows staged per CTA
 constexpr int BK = 64;                // bf16 elements per k-step (128 B rows)
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;  // 16 KB
-constexpr int B_BYTES = BN * BK * 2;  // 32 KB
+constexpr int STAGES = 6;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BNH * BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 256;
 constexpr int NTHREADS = 256;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*meta*/;
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // cluster smem address of CTA 0
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
@@ -56,12 +72,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2, int c3) {
+// 2-SM TMA: the bytes complete on the leader CTA's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1, int c2, int c3) {
   asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3)
       : "memory");
 }
 // K-major, 128B-swizzled UMMA shared-memory descriptor: SBO = 1024 B (8 rows
@@ -75,22 +93,26 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   desc |= (uint64_t)2 << 61;
   return desc;
 }
-// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N, M.
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, N = 256,
+// M = 256 (pair).
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
-                            ((uint32_t)(BM >> 4) << 24);
+                            ((uint32_t)((2 * BM) >> 4) << 24);
 
-__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t accum) {
+__device__ __forceinline__ void umma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accum));
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
+// completion of all prior MMAs arrives on the barrier at this offset in both CTAs
+__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -107,7 +129,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(NTHREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
               const float* __restrict__ knorm, const uint8_t* __restrict__ fusable,
               const uint8_t* __restrict__ alive, int32_t* __restrict__ absorber,
@@ -127,11 +149,14 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
   float* inv_j = reinterpret_cast<float*>(meta + 256);
   int32_t* colmin = reinterpret_cast<int32_t*>(meta + 256 + 4 * BN);
   uint8_t* ok_j = meta + 256 + 8 * BN;
-  double* red = reinterpret_cast<double*>(meta + 256 + 9 * BN);  // 4 warps x 5
+  double* red = reinterpret_cast<double*>(meta + 256 + 9 * BN);            // 4 warps x 5
   int32_t* colid = reinterpret_cast<int32_t*>(meta + 256 + 9 * BN + 256);  // block ids
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
+  const uint32_t crank = cta_rank();
+  const bool leader = crank == 0;
+  const int tile = blockIdx.x >> 1;
+  const int slot = blockIdx.x;  // partials slot (2 per tile)
   const int64_t ul = blockIdx.y, u = u0 + ul;
   const int64_t gb = u * g.NB;
   const int m = tiles[3 * tile], i0 = tiles[3 * tile + 1], j0 = tiles[3 * tile + 2];
@@ -147,22 +172,25 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
     pr = rk[re];
   }
   const int left_n = pm - pl, right_n = pr - pm;
-  if (i0 >= left_n || j0 >= right_n) {  // tile fully beyond the alive blocks
+  if (i0 >= left_n || j0 >= right_n) {  // tile fully beyond the alive blocks (both CTAs)
     if (threadIdx.x == 0) {
-      double* pp = partials + (ul * nt + tile) * 5;
+      double* pp = partials + ((int64_t)ul * gridDim.x + slot) * 5;
       pp[0] = pp[1] = pp[2] = 0.0;
       pp[3] = INFINITY;
       pp[4] = -INFINITY;
     }
     return;
   }
-  const int ni = min(BM, left_n - i0), nj = min(BN, right_n - j0);
+  const int mi0 = i0 + (int)crank * BM;          // this CTA's first A row in the merge
+  const int ni = max(0, min(BM, left_n - mi0));  // valid rows of this CTA
+  const int nj = min(BN, right_n - j0);
   const int layer = g.head_mode ? (int)(u / g.h) : (int)u;
   const int head = g.head_mode ? (int)(u % g.h) : 0;
   const int dpc = g.d / BK;
   const int nk = g.head_mode ? g.t * dpc : g.t * g.h * dpc;
-  const int rowA = staged ? (int)(ul * g.NB) + pl + i0 : (int)(layer * g.NB) + lb + i0;
-  const int rowB = staged ? (int)(ul * g.NB) + pm + j0 : (int)(layer * g.NB) + mid + j0;
+  const int rowA = staged ? (int)(ul * g.NB) + pl + mi0 : (int)(layer * g.NB) + lb + mi0;
+  const int rowB = (staged ? (int)(ul * g.NB) + pm + j0 : (int)(layer * g.NB) + mid + j0) +
+                   (int)crank * BNH;
   const int32_t* lv = live + gb;
 
   if (threadIdx.x == 0) {
@@ -172,13 +200,12 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
     }
     mbar_init(tmem_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   if (warp >= 3) {  // column metadata (160 threads cover 256 columns)
     for (int c = threadIdx.x - 96; c < BN; c += NTHREADS - 96) {
@@ -192,7 +219,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
@@ -211,14 +238,13 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
         const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
         uint8_t* sa = smem + s * STAGE_BYTES;
         uint8_t* sb = sa + A_BYTES;
-        mbar_expect_tx(&full_bar[s], STAGE_BYTES);
-        tma_load_4d(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
-        tma_load_4d(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
-        tma_load_4d(sb + A_BYTES, &tmap, &full_bar[s], c0, c1, c2, rowB + BM);
+        if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+        tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
+        tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (leader && lane == 0) {
       for (int ks = 0; ks < nk; ++ks) {
         const int s = ks % STAGES;
         const uint32_t ph = (ks / STAGES) & 1;
@@ -228,15 +254,16 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
         const uint32_t sb = sa + A_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / 16; ++k)
-          umma_bf16(tmem_base, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), (ks | k) != 0);
-        umma_commit(&empty_bar[s]);
+          umma_bf16_2sm(tmem_base, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32),
+                        (ks | k) != 0);
+        umma_commit_2sm(&empty_bar[s]);
       }
-      umma_commit(tmem_full);
+      umma_commit_2sm(tmem_full);
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
     const int row = ew * 32 + lane;
-    const int32_t my_id = row < ni ? (staged ? lv[pl + i0 + row] : lb + i0 + row) : 0;
+    const int32_t my_id = row < ni ? (staged ? lv[pl + mi0 + row] : lb + mi0 + row) : 0;
     const int64_t bi = gb + my_id;
     const bool ok_i = row < ni && alive[bi] && fusable[bi];
     const float ni_v = ok_i ? knorm[bi] : 0.f;
@@ -287,7 +314,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
       }
       if (mine != kNone) atomicMin(&colmin[c0 + lane], mine);
     }
-    // per-tile similarity moments: deterministic warp tree, then fixed warp order
+    // per-CTA similarity moments: deterministic warp tree, then fixed warp order
     double dc = cnt, d1 = s1, d2 = s2, dmn = mn, dmx = mx;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -318,15 +345,16 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
         o[3] = fmin(o[3], red[w * 5 + 3]);
         o[4] = fmax(o[4], red[w * 5 + 4]);
       }
-      double* pp = partials + (ul * nt + tile) * 5;
+      double* pp = partials + ((int64_t)ul * gridDim.x + slot) * 5;
       for (int q = 0; q < 5; ++q) pp[q] = o[q];
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  cluster_sync();  // both CTAs done with TMEM and smem before teardown
   if (warp == 2) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(TMEM_COLS));
   }
 }
@@ -404,10 +432,10 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   cuuint32_t box[4] = {(cuuint32_t)BK, 1, 1, (cuuint32_t)BM};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult res = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
-                            const_cast<void*>(staged ? a.staged : a.pool),
-                            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                              const_cast<void*>(staged ? a.staged : a.pool), dims, strides, box,
+                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
@@ -418,13 +446,11 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   }
   float thr = (float)a.thr;
   if ((double)thr > a.thr) thr = nextafterf(thr, -INFINITY);  // (float)s > thr_f <=> s > thr
-  dim3 grid(a.nt, (unsigned)a.nU);
-  sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(tmap, g, a.u0, (const float*)a.knorm, a.fusable,
-                                                   a.alive, a.absorber, a.merges, a.tiles, a.nt,
-                                                   thr, a.partials, a.samples, a.sample_off,
-                                                   a.sample_stride, a.live, a.rank, a.resc,
-                                                   a.resc_count, (int)a.resc_cap,
-                                                   (float)a.resc_band);
+  dim3 grid(2 * a.nt, (unsigned)a.nU);
+  sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
+      tmap, g, a.u0, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
+      a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
+      a.resc_count, (int)a.resc_cap, (float)a.resc_band);
   return cudaGetLastError();
 }
 

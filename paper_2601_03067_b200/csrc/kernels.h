@@ -65,9 +65,11 @@ cudaError_t launch_rescore(const RescoreArgs& a, cudaStream_t s);
 constexpr int kSimtTile = 64;
 cudaError_t launch_sim_simt(const SimArgs& a, cudaStream_t s);
 
-// tcgen05 path (bf16 only): tile 128 x kTcTileN
-constexpr int kTcTileM = 128;
+// tcgen05 path (bf16 only): one 256 x 256 tile per CTA pair (cta_group::2),
+// similarity partials written per CTA (2 slots per tile)
+constexpr int kTcTileM = 256;
 constexpr int kTcTileN = 256;
+constexpr int kTcPartialsPerTile = 2;
 bool tc_supported(const SimArgs& a, const char** why);
 cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s);
 

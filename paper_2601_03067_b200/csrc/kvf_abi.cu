@@ -84,18 +84,21 @@ int kvf_state_init(int dtype, int64_t U, int64_t NB, const void* knorm, uint8_t*
                      "kvf_state_init");
 }
 
-int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m, int* tile_n) {
-  if (!tile_m || !tile_n) return fail(KVF_ERR_INVALID, "null pointer");
+int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m, int* tile_n,
+                       int* partials_per_tile) {
+  if (!tile_m || !tile_n || !partials_per_tile) return fail(KVF_ERR_INVALID, "null pointer");
   if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
   if (path == KVF_PATH_TC) {
     if (dtype != BF16) return fail(KVF_ERR_INVALID, "tcgen05 path requires a bf16 pool");
     *tile_m = kTcTileM;
     *tile_n = kTcTileN;
+    *partials_per_tile = kTcPartialsPerTile;
     return KVF_OK;
   }
   if (path != KVF_PATH_SIMT) return fail(KVF_ERR_INVALID, "unknown path %d", path);
   *tile_m = kSimtTile;
   *tile_n = kSimtTile;
+  *partials_per_tile = 1;
   return KVF_OK;
 }
 

@@ -84,7 +84,7 @@ def block_norms(pool: torch.Tensor, geom: Geometry, stream=None) -> torch.Tensor
 class _PlanDevice:
     """Device copies of one plan's per-level arrays (uploaded once)."""
 
-    def __init__(self, plan: Plan, tm: int, tn: int, device):
+    def __init__(self, plan: Plan, tm: int, tn: int, ppt: int, device):
         self.levels = []
         for lv in plan.levels:
             tiles, tile_off = lv.tiling(tm, tn)
@@ -96,6 +96,8 @@ class _PlanDevice:
                     row_merge=torch.from_numpy(lv.row_merge.copy()).to(device),
                     tiles=torch.from_numpy(tiles.copy()).to(device),
                     tile_off=torch.from_numpy(tile_off.copy()).to(device),
+                    # offsets in partials slots (ppt slots per tile)
+                    tile_off_p=torch.from_numpy((tile_off * ppt).astype(np.int32)).to(device),
                     sample_off=torch.from_numpy(s_off).to(device),
                     nm=int(lv.merges.shape[0]),
                     nt=int(tiles.shape[0]),
@@ -104,20 +106,22 @@ class _PlanDevice:
             )
 
 
-def _plan_device(plan: Plan, tm: int, tn: int, device) -> _PlanDevice:
+def _plan_device(plan: Plan, tm: int, tn: int, ppt: int, device) -> _PlanDevice:
     cache = plan.__dict__.setdefault("_device_cache", {})
-    key = (tm, tn, str(device))
+    key = (tm, tn, ppt, str(device))
     if key not in cache:
-        cache[key] = _PlanDevice(plan, tm, tn, device)
+        cache[key] = _PlanDevice(plan, tm, tn, ppt, device)
     return cache[key]
 
 
-def tile_shape(dtype: torch.dtype, head_mode: int, path: int) -> tuple[int, int]:
+def tile_shape(dtype: torch.dtype, head_mode: int, path: int) -> tuple[int, int, int]:
+    """(tile_m, tile_n, partials slots per tile) of a similarity path."""
     import ctypes as C
 
-    tm, tn = C.c_int(), C.c_int()
-    N.call("kvf_sim_tile_shape", dtype_code(dtype), head_mode, path, C.byref(tm), C.byref(tn))
-    return tm.value, tn.value
+    tm, tn, ppt = C.c_int(), C.c_int(), C.c_int()
+    N.call("kvf_sim_tile_shape", dtype_code(dtype), head_mode, path, C.byref(tm), C.byref(tn),
+           C.byref(ppt))
+    return tm.value, tn.value, ppt.value
 
 
 @dataclass
@@ -164,12 +168,12 @@ class FusionEngine:
         if path == N.PATH_AUTO:
             path = N.PATH_TC if dtype == torch.bfloat16 and tc_available(geom) else N.PATH_SIMT
         self.path = path
-        self.tm, self.tn = tile_shape(dtype, geom.head_mode, path)
-        self.pdev = _plan_device(plan, self.tm, self.tn, self.device)
+        self.tm, self.tn, self.ppt = tile_shape(dtype, geom.head_mode, path)
+        self.pdev = _plan_device(plan, self.tm, self.tn, self.ppt, self.device)
         U, NB = geom.units, geom.NB
         dev = self.device
         max_nt = max([lv["nt"] for lv in self.pdev.levels], default=1)
-        self.partials = torch.empty((U, max(max_nt, 1), 5), dtype=torch.float64, device=dev)
+        self.partials = torch.empty((U, max(max_nt * self.ppt, 1), 5), dtype=torch.float64, device=dev)
         self.flag = torch.zeros(U * NB, dtype=torch.int32, device=dev)
         self.list = torch.empty(U * NB, dtype=torch.int32, device=dev)
         self.count = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -279,7 +283,7 @@ class FusionEngine:
             self.count.zero_()
             N.call(
                 "kvf_level_stats", 0, U, NB, N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber),
-                N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off"]), nt, N.ptr(self.partials),
+                N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt, N.ptr(self.partials),
                 N.ptr(stats), N.ptr(self.flag), N.ptr(self.list), N.ptr(self.count), sp,
             )
             N.call(
@@ -315,7 +319,7 @@ class FusionEngine:
 def tc_available(geom: Geometry) -> bool:
     """Whether the tcgen05 similarity path accepts this geometry (bf16 pools)."""
     try:
-        tm, tn = tile_shape(torch.bfloat16, geom.head_mode, N.PATH_TC)
+        tile_shape(torch.bfloat16, geom.head_mode, N.PATH_TC)
     except Exception:
         return False
     return _tc_geometry_ok(geom)
