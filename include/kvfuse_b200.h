@@ -114,41 +114,38 @@ int kvf_stage_rows(const void* pool, int dtype, int64_t L, int64_t NB, int t,
                    const int32_t* live, const int32_t* count, void* staged,
                    void* stream);
 
-/* Per-merge statistics of one level + absorber marking (MergeRecord,
+/* Level workspace: int32[kvf_level_ws_ints(U * NB)], zero-filled once before
+ * the first level (kvf_remap restores the zero invariant for the next one).
+ * Holds member counts / segments / ids per absorber and the absorber list. */
+int64_t kvf_level_ws_ints(int64_t n_total);
+
+/* Per-merge statistics of one level + member lists (MergeRecord,
  * fusion.py:93-110, 273-281). stats: double[nU][nm][8] = {left_blocks,
- * right_blocks, fused_count, n, sum, sumsq, min, max}. flag: int32[U][NB]
- * scratch (zero on entry); list: int32 global ids u*NB+l of this level's
- * absorbers, count_dev: int32[1] (zero on entry). */
-int kvf_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
-                    const uint8_t* alive, const int32_t* absorber,
-                    const int32_t* merges, int nm, const int32_t* tile_off,
-                    int nt, const double* partials, double* stats,
-                    int32_t* flag, int32_t* list, int32_t* count_dev,
-                    void* stream);
+ * right_blocks, fused_count, n, sum, sumsq, min, max}. For every absorber l
+ * of the level, the ascending ids j with absorber[j] == l (the `rids` of
+ * fusion.py:256-259) are written to the level workspace. */
+int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB,
+                    const uint8_t* fusable, const uint8_t* alive,
+                    const int32_t* absorber, const int32_t* merges, int nm,
+                    const int32_t* tile_off, int nt, const double* partials,
+                    double* stats, int32_t* level_ws, void* stream);
 
 /* K4 -- in-place block merge (replaces fusion.py:259-261, _unit 285-287):
  * for each absorber l, dir = unit(dir_l + sum_{j: absorber[j]=l} dir_j) for K
- * and the same indices for V; written back as s_home * dir with s_home the
- * home slot's original norm (1 if zero), stored norm recomputed.
- * Uses this level's kvf_level_stats outputs (member counts in `flag`,
- * absorber list/count) and the pre-remap `alive` flags.
- * row_merge: int32[rows] merge index of each row at this level (or -1).
- * workspace: int32[kvf_merge_workspace_ints(U*NB)]. */
-int64_t kvf_merge_workspace_ints(int64_t n_total);
+ * and the same indices for V (members summed in ascending order); written
+ * back as s_home * dir with s_home the home slot's original norm (1 if
+ * zero); stored norm recomputed from the rounded values. */
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L,
                      int64_t NB, int t, int h, int d, int head_mode, void* knorm,
                      void* vnorm, const void* orig_knorm, const void* orig_vnorm,
-                     const int32_t* absorber, const uint8_t* alive,
-                     const int32_t* merges, const int32_t* row_merge, int bpr,
-                     const int32_t* list, const int32_t* count_dev,
-                     const int32_t* flag, int32_t* workspace, int64_t list_cap,
-                     void* stream);
+                     int32_t* level_ws, void* stream);
 
 /* K5 -- block-table remap + refcounts (replaces BlockTable.redirect,
- * core.py:217-227, and alive[rid] = False, fusion.py:262-264). Clears flag. */
-int kvf_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber,
-              int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* flag,
-              void* stream);
+ * core.py:217-227, and alive[rid] = False, fusion.py:262-264); resets the
+ * level workspace counters. */
+int kvf_remap(int64_t u0, int64_t nU, int64_t U, int64_t NB,
+              const int32_t* absorber, int32_t* table, int32_t* refcount,
+              uint8_t* alive, int32_t* level_ws, void* stream);
 
 /* Finalize: per-slot scales k_scale[s] = orig_knorm[s] / knorm[table[s]]
  * (same for V; refold semantics core.py:303-304), ascending live list

@@ -51,17 +51,15 @@ SIGNATURES: dict[str, tuple] = {
     "kvf_stage_rows": (
         _i32, [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp]
     ),
+    "kvf_level_ws_ints": (_i64, [_i64]),
     "kvf_level_stats": (
         _i32,
-        [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp],
+        [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     ),
-    "kvf_merge_workspace_ints": (_i64, [_i64]),
     "kvf_merge_groups": (
-        _i32,
-        [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp,
-         _vp, _vp, _i32, _vp, _vp, _vp, _vp, _i64, _vp],
+        _i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
     ),
-    "kvf_remap": (_i32, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "kvf_remap": (_i32, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kvf_finalize": (
         _i32,
         [_i32, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

@@ -122,334 +122,10 @@ cudaError_t launch_state_init(int dtype, int64_t U, int64_t NB, const void* knor
 }
 
 // --------------------------------------------------------------------------
-// Level statistics + absorber marking: one CTA per (merge, unit).
-// --------------------------------------------------------------------------
-__global__ void level_stats_kernel(int64_t u0, int64_t NB, const uint8_t* __restrict__ fusable,
-                                   const uint8_t* __restrict__ alive,
-                                   const int32_t* __restrict__ absorber,
-                                   const int32_t* __restrict__ merges, int nm,
-                                   const int32_t* __restrict__ tile_off, int nt,
-                                   const double* __restrict__ partials, double* stats,
-                                   int32_t* flag, int32_t* list, int32_t* count) {
-  __shared__ double red[32];
-  const int m = blockIdx.x;
-  const int64_t ul = blockIdx.y, u = u0 + ul;
-  const int64_t gb = u * NB;
-  const int lb = merges[3 * m], mid = merges[3 * m + 1], re = merges[3 * m + 2];
-  double nl = 0, nr = 0, nf = 0;
-  for (int i = lb + threadIdx.x; i < mid; i += blockDim.x)
-    nl += (alive[gb + i] && fusable[gb + i]) ? 1.0 : 0.0;
-  for (int j = mid + threadIdx.x; j < re; j += blockDim.x) {
-    const bool al = alive[gb + j];
-    nr += (al && fusable[gb + j]) ? 1.0 : 0.0;
-    const int32_t a = absorber[gb + j];
-    if (al && a != kNone) {
-      nf += 1.0;
-      if (atomicAdd(&flag[gb + a], 1) == 0) {  // flag = member count of absorber a
-        const int pos = atomicAdd(count, 1);
-        list[pos] = (int32_t)(gb + a);
-      }
-    }
-  }
-  // similarity partials of this merge's tiles (fixed order => deterministic)
-  double c = 0, s1 = 0, s2 = 0, mn = INFINITY, mx = -INFINITY;
-  const double* pb = partials + ul * (int64_t)nt * 5;
-  for (int tt = tile_off[m] + threadIdx.x; tt < tile_off[m + 1]; tt += blockDim.x) {
-    const double* q = pb + (int64_t)tt * 5;
-    c += q[0];
-    s1 += q[1];
-    s2 += q[2];
-    mn = fmin(mn, q[3]);
-    mx = fmax(mx, q[4]);
-  }
-  nl = block_sum(nl, red);
-  nr = block_sum(nr, red);
-  nf = block_sum(nf, red);
-  c = block_sum(c, red);
-  s1 = block_sum(s1, red);
-  s2 = block_sum(s2, red);
-  // min / max are order independent
-  __shared__ double smn[32], smx[32];
-  for (int o = 16; o > 0; o >>= 1) {
-    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  }
-  if ((threadIdx.x & 31) == 0) {
-    smn[threadIdx.x >> 5] = mn;
-    smx[threadIdx.x >> 5] = mx;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      mn = fmin(mn, smn[w]);
-      mx = fmax(mx, smx[w]);
-    }
-    double* o = stats + (ul * nm + m) * 8;
-    o[0] = nl; o[1] = nr; o[2] = nf; o[3] = c; o[4] = s1; o[5] = s2;
-    o[6] = c > 0 ? mn : 0.0;
-    o[7] = c > 0 ? mx : 0.0;
-  }
-}
-
-cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
-                               const uint8_t* alive, const int32_t* absorber,
-                               const int32_t* merges, int nm, const int32_t* tile_off,
-                               int nt, const double* partials, double* stats,
-                               int32_t* flag, int32_t* list, int32_t* count, cudaStream_t s) {
-  if (nm == 0 || nU == 0) return cudaSuccess;
-  dim3 grid(nm, (unsigned)nU);
-  level_stats_kernel<<<grid, 256, 0, s>>>(u0, NB, fusable, alive, absorber, merges, nm,
-                                          tile_off, nt, partials, stats, flag, list, count);
-  return cudaGetLastError();
-}
-
-// --------------------------------------------------------------------------
-// K4: merge. Persistent grid (x = absorber list stride, y = 0:K / 1:V).
-// Member lists are bucketed per absorber (count -> segment -> scatter); each
-// CTA sorts its absorber's members ascending (rank sort in smem) so the fp
-// summation order is fixed and the result is bitwise deterministic. Groups
-// larger than the smem list fall back to an ordered scan of the right range.
-// --------------------------------------------------------------------------
-constexpr int kMaxSorted = 512;
-
-__global__ void member_seg_kernel(const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-                                  const int32_t* __restrict__ mcnt, int32_t* mstart,
-                                  int32_t* cursor) {
-  const int n = *count;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int32_t a = list[i];
-    mstart[a] = atomicAdd(cursor, mcnt[a]);
-  }
-}
-
-__global__ void member_scatter_kernel(int64_t n, int64_t NB, const uint8_t* __restrict__ alive,
-                                      const int32_t* __restrict__ absorber,
-                                      const int32_t* __restrict__ mstart, int32_t* mfill,
-                                      int32_t* members) {
-  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
-       x += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t aj = absorber[x];
-    if (aj != kNone && alive[x]) {
-      const int64_t a = (x / NB) * NB + aj;
-      const int slot = atomicAdd(&mfill[a], 1);
-      members[mstart[a] + slot] = (int32_t)(x % NB);
-    }
-  }
-}
-
-template <typename T, int VEC>
-__global__ void __launch_bounds__(512, 1)
-merge_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
-             typename AccOf<T>::type* __restrict__ knorm,
-             typename AccOf<T>::type* __restrict__ vnorm,
-             const typename AccOf<T>::type* __restrict__ oknorm,
-             const typename AccOf<T>::type* __restrict__ ovnorm,
-             const int32_t* __restrict__ absorber, const int32_t* __restrict__ merges,
-             const int32_t* __restrict__ row_merge, int bpr,
-             const int32_t* __restrict__ list, const int32_t* __restrict__ count,
-             const int32_t* __restrict__ mcnt, const int32_t* __restrict__ mstart,
-             const int32_t* __restrict__ members_g) {
-  using A = typename AccOf<T>::type;
-  constexpr int MAXQ = 32 / VEC;
-  __shared__ A red[32];
-  __shared__ int32_t raw[kMaxSorted];
-  __shared__ int32_t members[kMaxSorted];
-  __shared__ int warp_cnt[16];
-  __shared__ int nmem;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bd = blockDim.x;
-  const bool is_v = blockIdx.y == 1;
-  T* pool = is_v ? pool_v : pool_k;
-  A* norm = is_v ? vnorm : knorm;
-  const A* onorm = is_v ? ovnorm : oknorm;
-  const int64_t nch = g.r() / VEC;
-  const int n_items = *count;
-
-  auto accumulate = [&](A (&acc)[MAXQ][VEC], int64_t u, int n) {
-    const int64_t gb = u * g.NB;
-    for (int k = 0; k < n; ++k) {
-      const int32_t jm = members[k];
-      const A nj = norm[gb + jm];
-      const A inv = nj > A(0) ? A(1) / nj : A(0);
-      const T* xj = pool + g.base(u, jm);
-#pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int64_t c = tid + (int64_t)q * bd;
-        if (c < nch) {
-          A v[VEC];
-          VecIO<T, VEC>::load(xj + g.off(c * VEC), v);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[q][e] += v[e] * inv;
-        }
-      }
-    }
-  };
-
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int64_t gid = list[it];
-    const int64_t u = gid / g.NB;
-    const int32_t l = (int32_t)(gid % g.NB);
-    const int64_t gb = u * g.NB;
-    const int nmemb = mcnt[gid];
-    A acc[MAXQ][VEC];
-    {
-      const A nl = norm[gid];
-      const A inv = nl > A(0) ? A(1) / nl : A(0);
-      const T* xl = pool + g.base(u, l);
-#pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int64_t c = tid + (int64_t)q * bd;
-        if (c < nch) {
-          VecIO<T, VEC>::load(xl + g.off(c * VEC), acc[q]);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[q][e] *= inv;
-        } else {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[q][e] = A(0);
-        }
-      }
-    }
-    if (nmemb <= kMaxSorted) {
-      const int s0 = mstart[gid];
-      for (int k = tid; k < nmemb; k += bd) raw[k] = members_g[s0 + k];
-      __syncthreads();
-      for (int k = tid; k < nmemb; k += bd) {  // rank sort (ids are distinct)
-        const int32_t v = raw[k];
-        int rank = 0;
-        for (int q = 0; q < nmemb; ++q) rank += raw[q] < v;
-        members[rank] = v;
-      }
-      __syncthreads();
-      accumulate(acc, u, nmemb);
-      __syncthreads();
-    } else {
-      const int m = row_merge[l / bpr];
-      const int mid = merges[3 * m + 1], re = merges[3 * m + 2];
-      for (int j0 = mid; j0 < re; j0 += bd) {
-        const int j = j0 + tid;
-        const bool match = j < re && absorber[gb + j] == l;
-        const unsigned bal = __ballot_sync(0xffffffffu, match);
-        if (lane == 0) warp_cnt[warp] = __popc(bal);
-        __syncthreads();
-        if (tid == 0) {
-          int run = 0;
-          for (int w = 0; w < (bd >> 5); ++w) {
-            const int cnum = warp_cnt[w];
-            warp_cnt[w] = run;
-            run += cnum;
-          }
-          nmem = run;
-        }
-        __syncthreads();
-        if (match) members[warp_cnt[warp] + __popc(bal & ((1u << lane) - 1u))] = j;
-        __syncthreads();
-        accumulate(acc, u, nmem);
-        __syncthreads();
-      }
-    }
-    A ss = 0;
-#pragma unroll
-    for (int q = 0; q < MAXQ; ++q)
-#pragma unroll
-      for (int e = 0; e < VEC; ++e) ss += acc[q][e] * acc[q][e];
-    const A nrm = sqrt(block_sum(ss, red));
-    const A home = onorm[gid];
-    const A sc = nrm > A(0) ? (home > A(0) ? home : A(1)) / nrm : A(0);
-    T* xl = pool + g.base(u, l);
-    A rs = 0;
-#pragma unroll
-    for (int q = 0; q < MAXQ; ++q) {
-      const int64_t c = tid + (int64_t)q * bd;
-      if (c < nch) {
-        A v[VEC], rd[VEC];
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) v[e] = acc[q][e] * sc;
-        VecIO<T, VEC>::store(xl + g.off(c * VEC), v, rd);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) rs += rd[e] * rd[e];
-      }
-    }
-    const A nn = sqrt(block_sum(rs, red));
-    if (tid == 0) norm[gid] = nn;
-    __syncthreads();
-  }
-}
-
-struct MergeWs {  // int32 workspace: [mfill | cursor | pad | mstart | members]
-  int32_t *mfill, *cursor, *mstart, *members;
-  MergeWs(int32_t* ws, int64_t n) : mfill(ws), cursor(ws + n), mstart(ws + n + 32), members(ws + 2 * n + 32) {}
-};
-
-template <typename T, int VEC>
-static cudaError_t merge_t(void* pk, void* pv, const Geom& g, void* kn, void* vn,
-                           const void* okn, const void* ovn, const int32_t* absorber,
-                           const uint8_t* alive, const int32_t* merges, const int32_t* row_merge,
-                           int bpr, const int32_t* list, const int32_t* count, const int32_t* mcnt,
-                           int32_t* ws, int64_t cap, cudaStream_t s) {
-  using A = typename AccOf<T>::type;
-  const int64_t nch = g.r() / VEC;
-  int bd = 512;
-  while (bd > 64 && (int64_t)(bd / 2) * (32 / VEC) >= nch) bd /= 2;  // small vectors: small CTAs
-  if (nch > (int64_t)bd * (32 / VEC)) return cudaErrorInvalidValue;
-  const int64_t n = g.units() * g.NB;
-  MergeWs w(ws, n);
-  cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(int32_t) * (n + 1), s);
-  if (e != cudaSuccess) return e;
-  const int sgrid = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
-  member_seg_kernel<<<sgrid, 256, 0, s>>>(list, count, mcnt, w.mstart, w.cursor);
-  member_scatter_kernel<<<sgrid, 256, 0, s>>>(n, g.NB, alive, absorber, w.mstart, w.mfill,
-                                              w.members);
-  int64_t gx = cap < 148 * 4 ? cap : 148 * 4;
-  if (gx < 1) gx = 1;
-  dim3 grid((unsigned)gx, 2);
-  merge_kernel<T, VEC><<<grid, bd, 0, s>>>((T*)pk, (T*)pv, g, (A*)kn, (A*)vn, (const A*)okn,
-                                           (const A*)ovn, absorber, merges, row_merge, bpr,
-                                           list, count, mcnt, w.mstart, w.members);
-  return cudaGetLastError();
-}
-
-template <typename T>
-static cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn,
-                                  const void* okn, const void* ovn, const int32_t* absorber,
-                                  const uint8_t* alive, const int32_t* merges,
-                                  const int32_t* row_merge, int bpr, const int32_t* list,
-                                  const int32_t* count, const int32_t* mcnt, int32_t* ws,
-                                  int64_t cap, cudaStream_t s) {
-  if (can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g))
-    return merge_t<T, Vec16<T>::N>(pk, pv, g, kn, vn, okn, ovn, absorber, alive, merges,
-                                   row_merge, bpr, list, count, mcnt, ws, cap, s);
-  return merge_t<T, 1>(pk, pv, g, kn, vn, okn, ovn, absorber, alive, merges, row_merge, bpr,
-                       list, count, mcnt, ws, cap, s);
-}
-
-int64_t merge_workspace_ints(int64_t n_total) { return 3 * n_total + 64; }
-
-cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
-                                void* knorm, void* vnorm, const void* oknorm,
-                                const void* ovnorm, const int32_t* absorber,
-                                const uint8_t* alive, const int32_t* merges,
-                                const int32_t* row_merge, int bpr, const int32_t* list,
-                                const int32_t* count, const int32_t* mcnt, int32_t* ws,
-                                int64_t cap, cudaStream_t s) {
-  switch (dtype) {
-    case F64:
-      return merge_dispatch<double>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, absorber,
-                                    alive, merges, row_merge, bpr, list, count, mcnt, ws, cap, s);
-    case F32:
-      return merge_dispatch<float>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, absorber,
-                                   alive, merges, row_merge, bpr, list, count, mcnt, ws, cap, s);
-    default:
-      return merge_dispatch<__nv_bfloat16>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm,
-                                           absorber, alive, merges, row_merge, bpr, list, count,
-                                           mcnt, ws, cap, s);
-  }
-}
-
-// --------------------------------------------------------------------------
 // K5: remap. Slot s follows its block if that block was absorbed this level;
 // absorbed blocks hand their refcount to the absorber and die.
 // --------------------------------------------------------------------------
-__global__ void remap_kernel(int64_t u0, int64_t nU, int64_t NB,
+__global__ void remap_kernel(int64_t u0, int64_t nU, int64_t NB, int64_t n_total,
                              const int32_t* __restrict__ absorber, int32_t* table,
                              int32_t* refcount, uint8_t* alive, int32_t* flag) {
   const int64_t n = nU * NB;
@@ -466,17 +142,19 @@ __global__ void remap_kernel(int64_t u0, int64_t nU, int64_t NB,
       refcount[gb + s] = 0;
       alive[gb + s] = 0;
     }
-    flag[gb + s] = 0;
+    flag[gb + s] = 0;  // member count (LevelWs::mcnt)
+    flag[n_total + gb + s] = 0;  // member fill (LevelWs::mfill)
   }
 }
 
-cudaError_t launch_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber,
-                         int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* flag,
-                         cudaStream_t s) {
+cudaError_t launch_remap(int64_t u0, int64_t nU, int64_t NB, int64_t n_total,
+                         const int32_t* absorber, int32_t* table, int32_t* refcount,
+                         uint8_t* alive, int32_t* level_ws, cudaStream_t s) {
   const int64_t n = nU * NB;
   if (n == 0) return cudaSuccess;
   const int grid = (int)((n + 255) / 256 < 148 * 32 ? (n + 255) / 256 : 148 * 32);
-  remap_kernel<<<grid, 256, 0, s>>>(u0, nU, NB, absorber, table, refcount, alive, flag);
+  remap_kernel<<<grid, 256, 0, s>>>(u0, nU, NB, n_total, absorber, table, refcount, alive,
+                                    level_ws);
   return cudaGetLastError();
 }
 

@@ -1,0 +1,519 @@
+// Per-level bookkeeping and K4 (merge) of the fusion tree.
+//
+// level_stats (CTA per (merge, unit)):
+//   * MergeRecord counters (fusion.py:273-281): alive fusable left / right
+//     blocks, fused count, similarity moments reduced in fixed order from the
+//     similarity kernel's per-tile partials;
+//   * member lists: per absorber l of this merge, the ascending list of right
+//     blocks j with absorber[j] == l (the `rids` of fusion.py:256-259) built
+//     with an ordered, warp-sequential scatter, so every merge sums its members
+//     in ascending order -> bitwise deterministic results without sorting.
+// merge (K4, fusion.py:259-261, _unit 285-287): for each (absorber, K|V)
+//   dir = unit(dir_l + sum_j dir_j) rewritten in place as s_home * dir.
+//   Main path: persistent CTAs, one producer warp streaming every needed block
+//   vector into a shared-memory ring with cp.async.bulk (mbarrier complete_tx),
+//   eight consumer warps accumulating in registers (fp32) -> HBM-bound.
+//   Fallback (fp64 pools, unaligned pools): register-only CTA per item.
+#include <algorithm>
+#include <type_traits>
+#include "kernels.h"
+#include "vec_io.cuh"
+
+namespace kvf {
+
+// ---------------------------------------------------------------------------
+// level statistics + ordered member segments
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int LS_THREADS = 512;
+constexpr int LS_WARPS = LS_THREADS / 32;
+
+// deterministic block-exclusive scan of one int per thread; returns the
+// exclusive prefix, writes the block total to *total
+__device__ __forceinline__ int block_excl_scan(int v, int* wsum, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int w = 0; w < LS_WARPS; ++w) {
+      const int t = wsum[w];
+      wsum[w] = run;
+      run += t;
+    }
+    *total = run;
+  }
+  __syncthreads();
+  const int r = wsum[warp] + x - v;
+  __syncthreads();
+  return r;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(LS_THREADS)
+level_stats_kernel(int64_t u0, int64_t NB, int64_t n_total, const uint8_t* __restrict__ fusable,
+                   const uint8_t* __restrict__ alive, const int32_t* __restrict__ absorber,
+                   const int32_t* __restrict__ merges, int nm,
+                   const int32_t* __restrict__ tile_off, int nt,
+                   const double* __restrict__ partials, double* stats, int32_t* ws) {
+  __shared__ double red[32];
+  __shared__ int wsum[LS_WARPS];
+  __shared__ int tot_c, tot_f, run_c, lbase, seg_base;
+  LevelWs W(ws, n_total);
+  const int m = blockIdx.x;
+  const int64_t ul = blockIdx.y, u = u0 + ul;
+  const int64_t gb = u * NB;
+  const int lb = merges[3 * m], mid = merges[3 * m + 1], re = merges[3 * m + 2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  // pass A: counters + member counts per absorber
+  double nl = 0, nr = 0, nf = 0;
+  for (int i = lb + threadIdx.x; i < mid; i += blockDim.x)
+    nl += (alive[gb + i] && fusable[gb + i]) ? 1.0 : 0.0;
+  for (int j = mid + threadIdx.x; j < re; j += blockDim.x) {
+    const bool al = alive[gb + j];
+    nr += (al && fusable[gb + j]) ? 1.0 : 0.0;
+    const int32_t a = absorber[gb + j];
+    if (al && a != kNone) {
+      nf += 1.0;
+      atomicAdd(&W.mcnt[gb + a], 1);
+    }
+  }
+  nl = block_sum(nl, red);
+  nr = block_sum(nr, red);
+  nf = block_sum(nf, red);
+  if (threadIdx.x == 0) {
+    seg_base = nf > 0 ? atomicAdd(W.cursor, (int)nf) : 0;
+    run_c = 0;
+  }
+  __syncthreads();
+
+  // pass B: member segments + absorber list, ascending over the left range
+  if (nf > 0) {
+    for (int c0 = lb; c0 < mid; c0 += blockDim.x) {
+      const int i = c0 + threadIdx.x;
+      const int c = i < mid ? W.mcnt[gb + i] : 0;
+      const int oc = block_excl_scan(c, wsum, &tot_c);
+      const int of = block_excl_scan(c > 0 ? 1 : 0, wsum, &tot_f);
+      if (threadIdx.x == 0) lbase = tot_f > 0 ? atomicAdd(W.count, tot_f) : 0;
+      __syncthreads();
+      if (c > 0) {
+        W.mstart[gb + i] = seg_base + run_c + oc;
+        W.list[lbase + of] = (int32_t)(gb + i);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) run_c += tot_c;
+      __syncthreads();
+    }
+    // pass C: ordered scatter of members (warps take turns -> ascending j)
+    for (int c0 = mid; c0 < re; c0 += blockDim.x) {
+      const int j = c0 + threadIdx.x;
+      int key = -1 - lane;
+      if (j < re) {
+        const int32_t a = absorber[gb + j];
+        if (a != kNone && alive[gb + j]) key = a;
+      }
+      if (!__syncthreads_or(key >= 0)) continue;
+      for (int w = 0; w < LS_WARPS; ++w) {
+        if (warp == w) {
+          const unsigned grp = __match_any_sync(0xffffffffu, key);
+          if (key >= 0) {
+            const int leader = __ffs(grp) - 1;
+            int b = 0;
+            if (lane == leader) {
+              b = W.mfill[gb + key];
+              W.mfill[gb + key] = b + __popc(grp);
+            }
+            b = __shfl_sync(grp, b, leader);
+            W.members[W.mstart[gb + key] + b + __popc(grp & ((1u << lane) - 1u))] = j;
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+
+  // similarity moments of this merge's tiles (fixed order => deterministic)
+  double c = 0, s1 = 0, s2 = 0, mn = INFINITY, mx = -INFINITY;
+  const double* pb = partials + ul * (int64_t)nt * 5;
+  for (int tt = tile_off[m] + threadIdx.x; tt < tile_off[m + 1]; tt += blockDim.x) {
+    const double* q = pb + (int64_t)tt * 5;
+    c += q[0];
+    s1 += q[1];
+    s2 += q[2];
+    mn = fmin(mn, q[3]);
+    mx = fmax(mx, q[4]);
+  }
+  c = block_sum(c, red);
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  __shared__ double smn[LS_WARPS], smx[LS_WARPS];
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    smn[warp] = mn;
+    smx[warp] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < LS_WARPS; ++w) {
+      mn = fmin(mn, smn[w]);
+      mx = fmax(mx, smx[w]);
+    }
+    double* o = stats + (ul * nm + m) * 8;
+    o[0] = nl; o[1] = nr; o[2] = nf; o[3] = c; o[4] = s1; o[5] = s2;
+    o[6] = c > 0 ? mn : 0.0;
+    o[7] = c > 0 ? mx : 0.0;
+  }
+}
+
+cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_total,
+                               const uint8_t* fusable, const uint8_t* alive,
+                               const int32_t* absorber, const int32_t* merges, int nm,
+                               const int32_t* tile_off, int nt, const double* partials,
+                               double* stats, int32_t* level_ws, cudaStream_t s) {
+  LevelWs W(level_ws, n_total);
+  cudaError_t e = cudaMemsetAsync(W.count, 0, 2 * sizeof(int32_t), s);  // count, cursor
+  if (e != cudaSuccess || nm == 0 || nU == 0) return e;
+  dim3 grid(nm, (unsigned)nU);
+  level_stats_kernel<<<grid, LS_THREADS, 0, s>>>(u0, NB, n_total, fusable, alive, absorber,
+                                                 merges, nm, tile_off, nt, partials, stats,
+                                                 level_ws);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// K4 main path: bulk-copy ring + register accumulation
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int MG_CONSUMERS = 256;
+constexpr int MG_THREADS = MG_CONSUMERS + 32;
+constexpr int MG_MAX_BUF = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ float consumer_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, cw = (threadIdx.x >> 5) - 1;
+  v = warp_sum(v);
+  if (lane == 0) red[cw] = v;
+  asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+  float t = 0.f;
+#pragma unroll
+  for (int w = 0; w < MG_CONSUMERS / 32; ++w) t += red[w];
+  asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+  return t;
+}
+}  // namespace
+
+template <typename T, int EPT>
+__global__ void __launch_bounds__(MG_THREADS, 1)
+merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* __restrict__ knorm,
+                 float* __restrict__ vnorm, const float* __restrict__ oknorm,
+                 const float* __restrict__ ovnorm, int32_t* ws, int64_t n_total, int nbuf,
+                 int slot_bytes) {
+  constexpr int VEC = 16 / (int)sizeof(T);
+  constexpr int CPT = EPT / VEC;  // 16-byte chunks per consumer thread
+  extern __shared__ __align__(128) uint8_t msm[];
+  uint8_t* ring = msm;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nbuf * slot_bytes);
+  uint64_t* empty = full + MG_MAX_BUF;
+  float* red = reinterpret_cast<float*>(empty + MG_MAX_BUF);
+  const LevelWs W(ws, n_total);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t r = g.r();
+  const uint32_t vbytes = (uint32_t)(r * (int64_t)sizeof(T));
+  const int n_items = 2 * (*W.count);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nbuf; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], MG_CONSUMERS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: stream [x_l, members...] of every item
+      uint32_t q = 0;
+      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const int64_t gid = W.list[it >> 1];
+        const T* pool = (it & 1) ? pool_v : pool_k;
+        const int64_t u = gid / g.NB;
+        const int32_t l = (int32_t)(gid % g.NB);
+        const int n = W.mcnt[gid], s0 = W.mstart[gid];
+        for (int v = 0; v <= n; ++v, ++q) {
+          const int32_t id = v == 0 ? l : W.members[s0 + v - 1];
+          const int s = q % nbuf;
+          mbar_wait(&empty[s], ((q / nbuf) & 1) ^ 1);
+          mbar_expect_tx(&full[s], vbytes);
+          const T* src = pool + g.base(u, id);
+          uint8_t* dst = ring + (size_t)s * slot_bytes;
+          if (!g.head_mode) {
+            bulk_g2s(dst, src, vbytes, &full[s]);
+          } else {
+            const uint32_t segb = (uint32_t)(g.d * sizeof(T));
+            for (int tk = 0; tk < g.t; ++tk)
+              bulk_g2s(dst + tk * segb, src + (int64_t)tk * g.h * g.d, segb, &full[s]);
+          }
+        }
+      }
+    }
+    return;
+  }
+  // consumers
+  const int ct = threadIdx.x - 32;
+  const int64_t nch = r / VEC;
+  uint32_t q = 0;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int64_t gid = W.list[it >> 1];
+    const bool is_v = it & 1;
+    T* pool = is_v ? pool_v : pool_k;
+    float* norm = is_v ? vnorm : knorm;
+    const float* onorm = is_v ? ovnorm : oknorm;
+    const int64_t u = gid / g.NB;
+    const int64_t gb = u * g.NB;
+    const int32_t l = (int32_t)(gid % g.NB);
+    const int n = W.mcnt[gid], s0 = W.mstart[gid];
+    float acc[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) acc[e] = 0.f;
+    for (int v = 0; v <= n; ++v, ++q) {
+      const int32_t id = v == 0 ? l : W.members[s0 + v - 1];
+      const float nv = norm[gb + id];
+      const float inv = nv > 0.f ? 1.f / nv : 0.f;
+      const int s = q % nbuf;
+      mbar_wait(&full[s], (q / nbuf) & 1);
+      const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * slot_bytes);
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) {
+        const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+        if (c < nch) {
+          float x[VEC];
+          VecIO<T, VEC>::load(sp + c * VEC, x);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[k * VEC + e] = fmaf(x[e], inv, acc[k * VEC + e]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) ss = fmaf(acc[e], acc[e], ss);
+    const float nrm = sqrtf(consumer_sum(ss, red));
+    const float home = onorm[gid];
+    const float sc = nrm > 0.f ? (home > 0.f ? home : 1.f) / nrm : 0.f;
+    T* xl = pool + g.base(u, l);
+    float rs = 0.f;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+      const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+      if (c < nch) {
+        float y[VEC], rd[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = acc[k * VEC + e] * sc;
+        VecIO<T, VEC>::store(xl + g.off(c * VEC), y, rd);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) rs = fmaf(rd[e], rd[e], rs);
+      }
+    }
+    const float nn = sqrtf(consumer_sum(rs, red));
+    if (ct == 0) norm[gid] = nn;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 fallback: one CTA per (absorber, K|V), register accumulation, members
+// read from the ordered segments (fp64 pools, unaligned pools, large r)
+// ---------------------------------------------------------------------------
+template <typename T, int VEC>
+__global__ void __launch_bounds__(512)
+merge_reg_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
+                 typename AccOf<T>::type* __restrict__ knorm,
+                 typename AccOf<T>::type* __restrict__ vnorm,
+                 const typename AccOf<T>::type* __restrict__ oknorm,
+                 const typename AccOf<T>::type* __restrict__ ovnorm, int32_t* ws,
+                 int64_t n_total) {
+  using A = typename AccOf<T>::type;
+  constexpr int MAXQ = 32 / VEC;
+  __shared__ A red[32];
+  const LevelWs W(ws, n_total);
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const bool is_v = blockIdx.y == 1;
+  T* pool = is_v ? pool_v : pool_k;
+  A* norm = is_v ? vnorm : knorm;
+  const A* onorm = is_v ? ovnorm : oknorm;
+  const int64_t nch = g.r() / VEC;
+  const int n_items = *W.count;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const int64_t gid = W.list[it];
+    const int64_t u = gid / g.NB;
+    const int64_t gb = u * g.NB;
+    const int32_t l = (int32_t)(gid % g.NB);
+    const int n = W.mcnt[gid], s0 = W.mstart[gid];
+    A acc[MAXQ][VEC];
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[q][e] = A(0);
+    for (int v = 0; v <= n; ++v) {
+      const int32_t id = v == 0 ? l : W.members[s0 + v - 1];
+      const A nv = norm[gb + id];
+      const A inv = nv > A(0) ? A(1) / nv : A(0);
+      const T* x = pool + g.base(u, id);
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int64_t c = tid + (int64_t)q * bd;
+        if (c < nch) {
+          A y[VEC];
+          VecIO<T, VEC>::load(x + g.off(c * VEC), y);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc[q][e] += y[e] * inv;
+        }
+      }
+    }
+    A ss = 0;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) ss += acc[q][e] * acc[q][e];
+    const A nrm = sqrt(block_sum(ss, red));
+    const A home = onorm[gid];
+    const A sc = nrm > A(0) ? (home > A(0) ? home : A(1)) / nrm : A(0);
+    T* xl = pool + g.base(u, l);
+    A rs = 0;
+#pragma unroll
+    for (int q = 0; q < MAXQ; ++q) {
+      const int64_t c = tid + (int64_t)q * bd;
+      if (c < nch) {
+        A y[VEC], rd[VEC];
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] = acc[q][e] * sc;
+        VecIO<T, VEC>::store(xl + g.off(c * VEC), y, rd);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) rs += rd[e] * rd[e];
+      }
+    }
+    const A nn = sqrt(block_sum(rs, red));
+    if (tid == 0) norm[gid] = nn;
+    __syncthreads();
+  }
+}
+
+namespace {
+template <typename T, int VEC>
+cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
+                      const void* ovn, int32_t* ws, int64_t n_total, cudaStream_t s) {
+  using A = typename AccOf<T>::type;
+  const int64_t nch = g.r() / VEC;
+  int bd = 512;
+  while (bd > 64 && (int64_t)(bd / 2) * (32 / VEC) >= nch) bd /= 2;
+  if (nch > (int64_t)bd * (32 / VEC)) return cudaErrorInvalidValue;
+  dim3 grid(148 * 4, 2);
+  merge_reg_kernel<T, VEC><<<grid, bd, 0, s>>>((T*)pk, (T*)pv, g, (A*)kn, (A*)vn, (const A*)okn,
+                                               (const A*)ovn, ws, n_total);
+  return cudaGetLastError();
+}
+
+template <typename T, int EPT>
+cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
+                      const void* ovn, int32_t* ws, int64_t n_total, int nbuf, int slot_bytes,
+                      cudaStream_t s) {
+  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + 64;
+  static int attr = 0;  // per instantiation
+  if (attr < smem) {
+    cudaError_t e = cudaFuncSetAttribute(merge_tma_kernel<T, EPT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  merge_tma_kernel<T, EPT><<<148, MG_THREADS, smem, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn,
+                                                         (const float*)okn, (const float*)ovn, ws,
+                                                         n_total, nbuf, slot_bytes);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
+                           const void* ovn, int32_t* ws, int64_t n_total, cudaStream_t s) {
+  constexpr int VEC = Vec16<T>::N;
+  const int64_t r = g.r();
+  const int64_t vbytes = r * (int64_t)sizeof(T);
+  const int slot_bytes = (int)((vbytes + 127) / 128 * 128);
+  const int nbuf = (int)std::min<int64_t>(MG_MAX_BUF, (200 * 1024) / slot_bytes);
+  const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
+                      can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
+                      (g.d * (int64_t)sizeof(T)) % 16 == 0;
+  if constexpr (!std::is_same<T, double>::value) {
+    if (tma_ok) {
+      const int64_t ept = (r + MG_CONSUMERS - 1) / MG_CONSUMERS;
+      if (ept <= 8)
+        return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+      if (ept <= 16)
+        return merge_tma<T, 16>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+      if (ept <= 32)
+        return merge_tma<T, 32>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+      return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+    }
+  }
+  if (can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g))
+    return merge_reg<T, VEC>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, s);
+  return merge_reg<T, 1>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, s);
+}
+}  // namespace
+
+cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
+                                void* knorm, void* vnorm, const void* oknorm,
+                                const void* ovnorm, int32_t* level_ws, cudaStream_t s) {
+  const int64_t n_total = g.units() * g.NB;
+  switch (dtype) {
+    case F64:
+      return merge_dispatch<double>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, level_ws,
+                                    n_total, s);
+    case F32:
+      return merge_dispatch<float>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, level_ws,
+                                   n_total, s);
+    default:
+      return merge_dispatch<__nv_bfloat16>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm,
+                                           level_ws, n_total, s);
+  }
+}
+
+}  // namespace kvf

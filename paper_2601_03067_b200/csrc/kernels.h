@@ -73,27 +73,35 @@ constexpr int kTcPartialsPerTile = 2;
 bool tc_supported(const SimArgs& a, const char** why);
 cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s);
 
-cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
-                               const uint8_t* alive, const int32_t* absorber,
-                               const int32_t* merges, int nm, const int32_t* tile_off,
-                               int nt, const double* partials, double* stats,
-                               int32_t* flag, int32_t* list, int32_t* count, cudaStream_t s);
-int64_t merge_workspace_ints(int64_t n_total);
+// Per-level workspace shared by level_stats / merge / remap (int32 words):
+//   mcnt[n] member count per absorber   mfill[n] scatter cursor per absorber
+//   mstart[n] member segment start      members[n] member ids (ascending per absorber)
+//   list[n] absorber global ids          count (absorbers), cursor (members)
+// n = U * NB (all units). remap re-zeroes mcnt / mfill for the next level.
+struct LevelWs {
+  int32_t *mcnt, *mfill, *mstart, *members, *list, *count, *cursor;
+  __host__ __device__ LevelWs(int32_t* ws, int64_t n)
+      : mcnt(ws), mfill(ws + n), mstart(ws + 2 * n), members(ws + 3 * n), list(ws + 4 * n),
+        count(ws + 5 * n), cursor(ws + 5 * n + 1) {}
+  static int64_t ints(int64_t n) { return 5 * n + 64; }
+};
+
+cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_total,
+                               const uint8_t* fusable, const uint8_t* alive,
+                               const int32_t* absorber, const int32_t* merges, int nm,
+                               const int32_t* tile_off, int nt, const double* partials,
+                               double* stats, int32_t* level_ws, cudaStream_t s);
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
-                                const void* ovnorm, const int32_t* absorber,
-                                const uint8_t* alive, const int32_t* merges,
-                                const int32_t* row_merge, int bpr, const int32_t* list,
-                                const int32_t* count, const int32_t* mcnt, int32_t* ws,
-                                int64_t cap, cudaStream_t s);
+                                const void* ovnorm, int32_t* level_ws, cudaStream_t s);
 cudaError_t launch_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive,
                               int32_t* live, int32_t* rank, int32_t* count, cudaStream_t s);
 cudaError_t launch_stage_rows(const void* pool, int dtype, const Geom& g, int64_t u0, int64_t nU,
                               const int32_t* live, const int32_t* count, void* staged,
                               cudaStream_t s);
-cudaError_t launch_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber,
-                         int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* flag,
-                         cudaStream_t s);
+cudaError_t launch_remap(int64_t u0, int64_t nU, int64_t NB, int64_t n_total,
+                         const int32_t* absorber, int32_t* table, int32_t* refcount,
+                         uint8_t* alive, int32_t* level_ws, cudaStream_t s);
 cudaError_t launch_finalize(int dtype, int64_t u0, int64_t nU, int64_t NB, const void* okn,
                             const void* ovn, const void* kn, const void* vn,
                             const int32_t* table, const uint8_t* alive, void* ks, void* vs,

@@ -173,41 +173,36 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
   return cuda_status(launch_sim_simt(a, (cudaStream_t)stream), "kvf_similarity_select[simt]");
 }
 
-int kvf_level_stats(int64_t u0, int64_t nU, int64_t NB, const uint8_t* fusable,
+int64_t kvf_level_ws_ints(int64_t n_total) { return LevelWs::ints(n_total); }
+
+int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB, const uint8_t* fusable,
                     const uint8_t* alive, const int32_t* absorber, const int32_t* merges, int nm,
                     const int32_t* tile_off, int nt, const double* partials, double* stats,
-                    int32_t* flag, int32_t* list, int32_t* count_dev, void* stream) {
-  if (nm > 0 && nU > 0 && (!fusable || !alive || !absorber || !merges || !tile_off || !stats ||
-                           !flag || !list || !count_dev))
+                    int32_t* level_ws, void* stream) {
+  if (!level_ws) return fail(KVF_ERR_INVALID, "null level workspace");
+  if (u0 < 0 || nU < 0 || u0 + nU > U) return fail(KVF_ERR_INVALID, "bad unit range");
+  if (nm > 0 && nU > 0 && (!fusable || !alive || !absorber || !merges || !tile_off || !stats))
     return fail(KVF_ERR_INVALID, "null pointer");
-  return cuda_status(launch_level_stats(u0, nU, NB, fusable, alive, absorber, merges, nm,
-                                        tile_off, nt, partials, stats, flag, list, count_dev,
+  return cuda_status(launch_level_stats(u0, nU, NB, U * NB, fusable, alive, absorber, merges, nm,
+                                        tile_off, nt, partials, stats, level_ws,
                                         (cudaStream_t)stream),
                      "kvf_level_stats");
 }
 
-int64_t kvf_merge_workspace_ints(int64_t n_total) { return merge_workspace_ints(n_total); }
-
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t NB, int t, int h,
                      int d, int head_mode, void* knorm, void* vnorm, const void* orig_knorm,
-                     const void* orig_vnorm, const int32_t* absorber, const uint8_t* alive,
-                     const int32_t* merges, const int32_t* row_merge, int bpr,
-                     const int32_t* list, const int32_t* count_dev, const int32_t* flag,
-                     int32_t* workspace, int64_t list_cap, void* stream) {
+                     const void* orig_vnorm, int32_t* level_ws, void* stream) {
   Geom g;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
   if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
-  if (bpr < 1) return fail(KVF_ERR_INVALID, "bpr must be >= 1");
-  if (!pool_k || !pool_v || !knorm || !vnorm || !absorber || !alive || !list || !count_dev ||
-      !flag || !workspace)
+  if (!pool_k || !pool_v || !knorm || !vnorm || !orig_knorm || !orig_vnorm || !level_ws)
     return fail(KVF_ERR_INVALID, "null pointer");
   const int64_t r = g.r();
   if (r > 16384)
     return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's 16384",
                 (long long)r);
   cudaError_t e = launch_merge_groups(pool_k, pool_v, dtype, g, knorm, vnorm, orig_knorm,
-                                      orig_vnorm, absorber, alive, merges, row_merge, bpr, list,
-                                      count_dev, flag, workspace, list_cap, (cudaStream_t)stream);
+                                      orig_vnorm, level_ws, (cudaStream_t)stream);
   return cuda_status(e, "kvf_merge_groups");
 }
 
@@ -231,11 +226,15 @@ int kvf_stage_rows(const void* pool, int dtype, int64_t L, int64_t NB, int t, in
       "kvf_stage_rows");
 }
 
-int kvf_remap(int64_t u0, int64_t nU, int64_t NB, const int32_t* absorber, int32_t* table,
-              int32_t* refcount, uint8_t* alive, int32_t* flag, void* stream) {
-  return cuda_status(
-      launch_remap(u0, nU, NB, absorber, table, refcount, alive, flag, (cudaStream_t)stream),
-      "kvf_remap");
+int kvf_remap(int64_t u0, int64_t nU, int64_t U, int64_t NB, const int32_t* absorber,
+              int32_t* table, int32_t* refcount, uint8_t* alive, int32_t* level_ws,
+              void* stream) {
+  if (!absorber || !table || !refcount || !alive || !level_ws)
+    return fail(KVF_ERR_INVALID, "null pointer");
+  if (u0 < 0 || nU < 0 || u0 + nU > U) return fail(KVF_ERR_INVALID, "bad unit range");
+  return cuda_status(launch_remap(u0, nU, NB, U * NB, absorber, table, refcount, alive, level_ws,
+                                  (cudaStream_t)stream),
+                     "kvf_remap");
 }
 
 int kvf_finalize(int dtype, int64_t u0, int64_t nU, int64_t NB, const void* orig_knorm,

@@ -174,10 +174,8 @@ class FusionEngine:
         dev = self.device
         max_nt = max([lv["nt"] for lv in self.pdev.levels], default=1)
         self.partials = torch.empty((U, max(max_nt * self.ppt, 1), 5), dtype=torch.float64, device=dev)
-        self.flag = torch.zeros(U * NB, dtype=torch.int32, device=dev)
-        self.list = torch.empty(U * NB, dtype=torch.int32, device=dev)
-        self.count = torch.zeros(1, dtype=torch.int32, device=dev)
-        self.merge_ws = torch.empty(int(N.lib().kvf_merge_workspace_ints(U * NB)), dtype=torch.int32,
+        # member counts / segments / absorber list of the current level
+        self.level_ws = torch.zeros(int(N.lib().kvf_level_ws_ints(U * NB)), dtype=torch.int32,
                                     device=dev)
         # compaction of the top levels (tcgen05 path): dead blocks dominate the
         # upper merges' rectangles, so their alive K rows are staged densely
@@ -246,7 +244,6 @@ class FusionEngine:
             g, self.plan, threshold, pool_k, pool_v, knorm, vnorm, oknorm, ovnorm, fusable,
             alive_t, absorber, table_t, ref_t,
         )
-        self.flag.zero_()
         for li, lv in enumerate(self.pdev.levels):
             nm, nt = lv["nm"], lv["nt"]
             stats = torch.empty((U, nm, 8), dtype=torch.float64, device=dev)
@@ -280,23 +277,20 @@ class FusionEngine:
             if time_sim:
                 e1.record(stream)
                 st.sim_events.append((e0, e1, li))
-            self.count.zero_()
             N.call(
-                "kvf_level_stats", 0, U, NB, N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber),
-                N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt, N.ptr(self.partials),
-                N.ptr(stats), N.ptr(self.flag), N.ptr(self.list), N.ptr(self.count), sp,
+                "kvf_level_stats", 0, U, U, NB, N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber),
+                N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt,
+                N.ptr(self.partials), N.ptr(stats), N.ptr(self.level_ws), sp,
             )
             N.call(
                 "kvf_merge_groups", N.ptr(pool_k), N.ptr(pool_v), dt, *g.args(), N.ptr(knorm),
-                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(absorber), N.ptr(alive_t),
-                N.ptr(lv["merges"]), N.ptr(lv["row_merge"]), self.plan.bpr, N.ptr(self.list),
-                N.ptr(self.count), N.ptr(self.flag), N.ptr(self.merge_ws), U * NB, sp,
+                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws), sp,
             )
             N.call(
-                "kvf_remap", 0, U, NB, N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t),
-                N.ptr(alive_t), N.ptr(self.flag), sp,
+                "kvf_remap", 0, U, U, NB, N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t),
+                N.ptr(alive_t), N.ptr(self.level_ws), sp,
             )
-            launches += 6
+            launches += 3
             st.level_stats.append(stats)
             st.level_samples.append(samples)
         st.k_scale = torch.empty((U, NB), dtype=acc, device=dev)
