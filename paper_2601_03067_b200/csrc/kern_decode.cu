@@ -7,7 +7,6 @@
 // Split-K (flash-decoding): CTA = (request, kv head, split of CB blocks),
 // online softmax per query head of the GQA group, then a combine kernel.
 #include "kernels.h"
-#include <cstdlib>
 #include <type_traits>
 #include "vec_io.cuh"
 
@@ -385,305 +384,7 @@ static cudaError_t decode_fast_t(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------------------
-// Tensor-core path (bf16 pools, d in {64, 128}, G <= 8): flash-decoding with
-// mma.sync m16n8k16 (bf16 in, fp32 accumulate). CTA = (split of CB blocks,
-// kv head, request), 8 warps x one 32-token tile each. Per warp:
-//   S^T = Q (G rows padded to 16) x K^T  -- K fragments via ldmatrix
-//   online softmax per query head across the 4 lanes of a row group
-//   O  += (P * v_scale) x V             -- P reused from the S accumulators,
-//                                          V fragments via ldmatrix.trans
-// Per-slot k_scale multiplies the logits, v_scale folds into P, so shared
-// fused blocks are read as stored. The 8 warp partials are merged in smem
-// into the same (o, m, l) split partial the combine kernel consumes.
-// ---------------------------------------------------------------------------
-namespace {
-constexpr int MMA_WARPS = 4;  // 71 KB smem per CTA -> 3 CTAs / SM
-constexpr int MMA_TT = 32;  // tokens per warp tile
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                        uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
-                                          uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-// D = A(16x16, rows >= 8 zero) x B(16x8) + D ; a1 / a3 (rows 8..15) are zero
-__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a2, uint32_t b0,
-                                         uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-}  // namespace
-
-template <int D, int TILES>
-__global__ void __launch_bounds__(MMA_WARPS * 32)
-decode_mma_kernel(const void* __restrict__ q, int q_dtype, const __nv_bfloat16* __restrict__ pool_k,
-                  const __nv_bfloat16* __restrict__ pool_v, Geom g, int64_t layer,
-                  const int32_t* __restrict__ table, const float* __restrict__ k_scale,
-                  const float* __restrict__ v_scale, int64_t p_blocks,
-                  const int32_t* __restrict__ seq_blocks, int Hq, float sm_scale,
-                  float* __restrict__ part) {
-  constexpr int ROWB = D * 2 + 16;  // padded row bytes (conflict-free ldmatrix)
-  constexpr int CPR = D * 2 / 16;   // 16-byte chunks per row
-  constexpr int KS = D / 16;        // k-steps over the head dim
-  constexpr int NE = D / 8;         // n-tiles over the head dim (PV)
-  constexpr int SBYTES = 2 * MMA_TT * ROWB + 2 * MMA_TT * 4;  // one stage
-  extern __shared__ __align__(16) uint8_t dsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int grp = lane >> 2, tig = lane & 3;
-  uint8_t* wsm = dsm + warp * 2 * SBYTES;  // this warp's 2 stages
-
-  const int G = Hq / g.h;
-  const int64_t b = blockIdx.z;
-  const int kvh = blockIdx.y;
-  const int64_t split = blockIdx.x, nsplit = gridDim.x;
-  const int64_t unit = g.head_mode ? layer * g.h + kvh : layer;
-  const int32_t* tab = table + unit * g.NB;
-  const float* ksc = k_scale + unit * g.NB;
-  const float* vsc = v_scale + unit * g.NB;
-  const int64_t nblk = seq_blocks ? (int64_t)seq_blocks[b] : p_blocks;
-  const int64_t span = (int64_t)MMA_WARPS * MMA_TT * TILES;  // tokens per split
-  const int64_t T1 = min((split + 1) * span, nblk * g.t);
-  const int64_t E = g.E();
-  const int64_t rstride = (int64_t)g.h * D;
-  // warp w owns tiles w, w + MMA_WARPS, ... of the split
-  auto tile_start = [&](int i) { return split * span + (int64_t)(i * MMA_WARPS + warp) * MMA_TT; };
-
-  auto issue = [&](int i) {
-    uint8_t* st = wsm + (i & 1) * SBYTES;
-    uint8_t* ksm = st;
-    uint8_t* vsm = st + MMA_TT * ROWB;
-    float* sks = reinterpret_cast<float*>(st + 2 * MMA_TT * ROWB);
-    float* svs = sks + MMA_TT;
-    const int64_t t0 = tile_start(i);  // multiple of t: the tile spans MMA_TT / t whole blocks
-    // one lane per block of the tile resolves table + scales (no dependent
-    // global loads inside the copy loop)
-    int64_t phys_l = 0;
-    float ks_l = 0.f, vs_l = 0.f;
-    const int nbt = MMA_TT / g.t;
-    if (lane < nbt) {
-      const int64_t blk = t0 / g.t + lane;
-      if (blk * g.t < T1) {
-        const int64_t slot = b * p_blocks + blk;
-        phys_l = tab[slot];
-        ks_l = ksc[slot] * sm_scale;
-        vs_l = vsc[slot];
-      }
-    }
-    for (int c = lane; c < MMA_TT * CPR; c += 32) {
-      const int row = c / CPR, col = c % CPR;
-      const int bl = row / g.t;
-      const int64_t phys = __shfl_sync(0xffffffffu, phys_l, bl);
-      const bool valid = t0 + row < T1;
-      const int64_t off = (layer * g.NB + phys) * E + (row % g.t) * rstride + (int64_t)kvh * D;
-      cp_async16(ksm + row * ROWB + col * 16,
-                 reinterpret_cast<const uint8_t*>(pool_k + off) + col * 16, valid);
-      cp_async16(vsm + row * ROWB + col * 16,
-                 reinterpret_cast<const uint8_t*>(pool_v + off) + col * 16, valid);
-    }
-    {
-      const bool valid = t0 + lane < T1;
-      const float kk = __shfl_sync(0xffffffffu, ks_l, lane / g.t);
-      const float vv = __shfl_sync(0xffffffffu, vs_l, lane / g.t);
-      sks[lane] = valid ? kk : 0.f;
-      svs[lane] = valid ? vv : 0.f;
-    }
-    cp_commit();
-  };
-
-  issue(0);
-  // ---- Q fragments (rows = query heads of the group, zero beyond G) ----
-  uint32_t qa[KS][2];
-  {
-    const bool real = grp < G;
-    const int64_t qrow = (b * Hq + (int64_t)kvh * G + (real ? grp : 0)) * D;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const int e0 = ks * 16 + 2 * tig;
-      float x0 = 0.f, x1 = 0.f, x8 = 0.f, x9 = 0.f;
-      if (real) {
-        if (q_dtype == BF16) {
-          const __nv_bfloat16* qp = (const __nv_bfloat16*)q + qrow;
-          x0 = __bfloat162float(qp[e0]);
-          x1 = __bfloat162float(qp[e0 + 1]);
-          x8 = __bfloat162float(qp[e0 + 8]);
-          x9 = __bfloat162float(qp[e0 + 9]);
-        } else {
-          const float* qp = (const float*)q + qrow;
-          x0 = qp[e0];
-          x1 = qp[e0 + 1];
-          x8 = qp[e0 + 8];
-          x9 = qp[e0 + 9];
-        }
-      }
-      qa[ks][0] = pack_bf16(x0, x1);
-      qa[ks][1] = pack_bf16(x8, x9);
-    }
-  }
-
-  float m_run = -INFINITY, l_run = 0.f;
-  float o[NE][4];
-#pragma unroll
-  for (int et = 0; et < NE; ++et)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) o[et][k] = 0.f;
-  const int lr = lane & 7, lm = lane >> 3;  // ldmatrix row / matrix index
-
-  for (int i = 0; i < TILES; ++i) {
-    if (i + 1 < TILES) {
-      issue(i + 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncwarp();
-    const uint8_t* st = wsm + (i & 1) * SBYTES;
-    const uint32_t kbase = static_cast<uint32_t>(__cvta_generic_to_shared(st));
-    const uint32_t vbase = kbase + MMA_TT * ROWB;
-    const float* sks = reinterpret_cast<const float*>(st + 2 * MMA_TT * ROWB);
-    const float* svs = sks + MMA_TT;
-    const int64_t t0 = tile_start(i);
-    // ---- S = Q K^T over 4 n-tiles of 8 tokens ----
-    float s[4][4];
-#pragma unroll
-    for (int n = 0; n < 4; ++n)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) s[n][k] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-#pragma unroll
-      for (int n = 0; n < 4; n += 2) {
-        // matrices: (tok n*8, e), (tok n*8, e + 8), (tok n*8 + 8, e), (tok n*8 + 8, e + 8)
-        const int tok = n * 8 + (lm >> 1) * 8 + lr;
-        const int e = ks * 16 + (lm & 1) * 8;
-        uint32_t r0, r1, r2, r3;
-        ldsm_x4(kbase + tok * ROWB + e * 2, r0, r1, r2, r3);
-        mma16816(s[n], qa[ks][0], qa[ks][1], r0, r1);
-        mma16816(s[n + 1], qa[ks][0], qa[ks][1], r2, r3);
-      }
-    }
-    // ---- online softmax (row = query head grp; 8 tokens per lane) ----
-    float mx = -INFINITY;
-#pragma unroll
-    for (int n = 0; n < 4; ++n)
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const int tl = n * 8 + 2 * tig + k;
-        const float lg = (t0 + tl < T1) ? s[n][k] * sks[tl] : -INFINITY;
-        s[n][k] = lg;
-        mx = fmaxf(mx, lg);
-      }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float m_new = fmaxf(m_run, mx);
-    const float alpha = m_new == -INFINITY ? 1.f : __expf(m_run - m_new);
-    float lsum = 0.f;
-#pragma unroll
-    for (int n = 0; n < 4; ++n)
-#pragma unroll
-      for (int k = 0; k < 2; ++k) {
-        const float p = m_new == -INFINITY ? 0.f : __expf(s[n][k] - m_new);
-        s[n][k] = p;
-        lsum += p;
-      }
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, 1);
-    lsum += __shfl_xor_sync(0xffffffffu, lsum, 2);
-    l_run = l_run * alpha + lsum;
-    m_run = m_new;
-#pragma unroll
-    for (int et = 0; et < NE; ++et) {
-      o[et][0] *= alpha;
-      o[et][1] *= alpha;
-    }
-    // ---- O += (P * v_scale) V ----
-#pragma unroll
-    for (int kk = 0; kk < 2; ++kk) {
-      const int tt = kk * 16 + 2 * tig;
-      const uint32_t a0 = pack_bf16(s[2 * kk][0] * svs[tt], s[2 * kk][1] * svs[tt + 1]);
-      const uint32_t a2 = pack_bf16(s[2 * kk + 1][0] * svs[tt + 8], s[2 * kk + 1][1] * svs[tt + 9]);
-#pragma unroll
-      for (int et = 0; et < NE; et += 2) {
-        // matrices: (tok kk*16, e et*8), (tok + 8, e), (tok, e + 8), (tok + 8, e + 8)
-        const int tok = kk * 16 + (lm & 1) * 8 + lr;
-        const int e = et * 8 + (lm >> 1) * 8;
-        uint32_t r0, r1, r2, r3;
-        ldsm_x4_t(vbase + tok * ROWB + e * 2, r0, r1, r2, r3);
-        mma16816(o[et], a0, a2, r0, r1);
-        mma16816(o[et + 1], a0, a2, r2, r3);
-      }
-    }
-    __syncwarp();  // stage (i & 1) is refilled by issue(i + 2)
-  }
-  // ---- merge the warp partials of this split ----
-  __syncthreads();  // stage smem reused below
-  float* wm = reinterpret_cast<float*>(dsm);  // [warps][8]
-  float* wl = wm + MMA_WARPS * 8;              // [warps][8]
-  float* wo = wl + MMA_WARPS * 8;              // [warps][8][D]
-  if (grp < G) {
-    if (tig == 0) {
-      wm[warp * 8 + grp] = m_run;
-      wl[warp * 8 + grp] = l_run;
-    }
-#pragma unroll
-    for (int et = 0; et < NE; ++et) {
-      wo[(warp * 8 + grp) * D + et * 8 + 2 * tig] = o[et][0];
-      wo[(warp * 8 + grp) * D + et * 8 + 2 * tig + 1] = o[et][1];
-    }
-  }
-  __syncthreads();
-  for (int x = threadIdx.x; x < G * D; x += MMA_WARPS * 32) {
-    const int gg = x / D, e = x % D;
-    float M = -INFINITY;
-    for (int w = 0; w < MMA_WARPS; ++w) M = fmaxf(M, wm[w * 8 + gg]);
-    float L = 0.f, O = 0.f;
-    for (int w = 0; w < MMA_WARPS; ++w) {
-      const float f = wm[w * 8 + gg] == -INFINITY ? 0.f : __expf(wm[w * 8 + gg] - M);
-      L += wl[w * 8 + gg] * f;
-      O += wo[(w * 8 + gg) * D + e] * f;
-    }
-    float* pp = part + (((b * Hq + (int64_t)kvh * G + gg) * nsplit) + split) * (D + 2);
-    pp[e] = O;
-    if (e == 0) {
-      pp[D] = M;
-      pp[D + 1] = L;
-    }
-  }
-}
-
-template <int D, int TILES>
-static cudaError_t decode_mma_t(const DecodeArgs& a, cudaStream_t s) {
-  constexpr int SBYTES = 2 * MMA_TT * (D * 2 + 16) + 2 * MMA_TT * 4;
-  constexpr int SMEM = MMA_WARPS * 2 * SBYTES;
-  static_assert(SMEM >= (2 * MMA_WARPS * 8 + MMA_WARPS * 8 * D) * 4, "combine area");
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(decode_mma_kernel<D, TILES>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int cbs = MMA_WARPS * MMA_TT * TILES / a.g.t;  // blocks per split
-  const int64_t nsplit = nsplit_of(a.p_blocks, cbs);
-  dim3 grid((unsigned)nsplit, a.g.h, (unsigned)a.B);
-  decode_mma_kernel<D, TILES><<<grid, MMA_WARPS * 32, SMEM, s>>>(
-      a.q, a.q_dtype, (const __nv_bfloat16*)a.pool_k, (const __nv_bfloat16*)a.pool_v, a.g,
-      a.layer, a.table, (const float*)a.k_scale, (const float*)a.v_scale, a.p_blocks,
-      a.seq_blocks, a.Hq, (float)a.sm_scale, (float*)a.ws);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+cudaError_t launch_decode_combine(const DecodeArgs& a, int64_t nsplit, int cbs, cudaStream_t s) {
   decode_combine_kernel<float><<<(unsigned)(a.B * a.Hq), 128, 0, s>>>(
       (const float*)a.ws, nsplit, a.g.d, a.p_blocks, a.g.t, a.seq_blocks, a.Hq, (float*)a.out,
       (float*)a.lse, nullptr, cbs);
@@ -693,30 +394,9 @@ static cudaError_t decode_mma_t(const DecodeArgs& a, cudaStream_t s) {
 template <typename T>
 static cudaError_t decode_t(const DecodeArgs& a, cudaStream_t s) {
   using A = typename AccOf<T>::type;
-  // the warps' 32-token tiles must cover whole blocks of a split
-  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    const bool qok = a.q_dtype == BF16 || a.q_dtype == F32;
-    // 32-token tiles per warp (double-buffered); KVF_DECODE_TILES overrides
-    static const int tiles = [] {
-      const char* e = getenv("KVF_DECODE_TILES");
-      const int v = e ? atoi(e) : 2;
-      return (v == 1 || v == 2 || v == 4) ? v : 2;
-    }();
-    const int span = MMA_WARPS * MMA_TT * tiles;
-    if (qok && a.probs == nullptr && MMA_TT % a.g.t == 0 && span / a.g.t >= CB_MIN &&
-        a.Hq / a.g.h <= 8) {
-      if (a.g.d == 128) {
-        if (tiles == 1) return decode_mma_t<128, 1>(a, s);
-        if (tiles == 2) return decode_mma_t<128, 2>(a, s);
-        return decode_mma_t<128, 4>(a, s);
-      }
-      if (a.g.d == 64) {
-        if (tiles == 1) return decode_mma_t<64, 1>(a, s);
-        if (tiles == 2) return decode_mma_t<64, 2>(a, s);
-        return decode_mma_t<64, 4>(a, s);
-      }
-    }
-  }
+  // bf16: TMA + mma.sync path; f32 (and bf16 shapes TMA cannot take): CUDA-core
+  // cp.async path; f64 / probability output: the generic kernel
+  if (decode_tma_supported(a)) return launch_decode_tma(a, s);
   if constexpr (!std::is_same<T, double>::value) {
     const bool qok = a.q_dtype == BF16 || a.q_dtype == F32;
     if (qok && (a.g.d == 128 || a.g.d == 64)) {

@@ -143,5 +143,9 @@ struct DecodeArgs {
   int64_t ws_bytes;
 };
 cudaError_t launch_paged_decode(const DecodeArgs& a, cudaStream_t s);
+// TMA + mma.sync decode path (kern_decode_tma.cu) and the shared split combine
+bool decode_tma_supported(const DecodeArgs& a);
+cudaError_t launch_decode_tma(const DecodeArgs& a, cudaStream_t s);
+cudaError_t launch_decode_combine(const DecodeArgs& a, int64_t nsplit, int cbs, cudaStream_t s);
 
 }  // namespace kvf
