@@ -241,6 +241,14 @@ __device__ __forceinline__ float consumer_sum(float v, float* red) {
 }
 }  // namespace
 
+// Per-slot metadata handed from the producer to the consumers with the data
+struct SlotMeta {
+  float inv;   // 1 / stored norm of the vector in the slot (0 for zero vectors)
+  float home;  // item: original norm of the absorber's home slot
+  int32_t gid; // item: global absorber id u * NB + l
+  int32_t flags;  // bit0: last vector of the item, bit1: V tensor
+};
+
 template <typename T, int EPT>
 __global__ void __launch_bounds__(MG_THREADS, 1)
 merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* __restrict__ knorm,
@@ -253,7 +261,8 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
   uint8_t* ring = msm;
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nbuf * slot_bytes);
   uint64_t* empty = full + MG_MAX_BUF;
-  float* red = reinterpret_cast<float*>(empty + MG_MAX_BUF);
+  SlotMeta* meta = reinterpret_cast<SlotMeta*>(empty + MG_MAX_BUF);
+  float* red = reinterpret_cast<float*>(meta + MG_MAX_BUF);
   const LevelWs W(ws, n_total);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = g.r();
@@ -270,19 +279,67 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
   __syncthreads();
 
   if (warp == 0) {
-    if (lane == 0) {  // producer: stream [x_l, members...] of every item
-      uint32_t q = 0;
-      for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-        const int64_t gid = W.list[it >> 1];
-        const T* pool = (it & 1) ? pool_v : pool_k;
-        const int64_t u = gid / g.NB;
-        const int32_t l = (int32_t)(gid % g.NB);
-        const int n = W.mcnt[gid], s0 = W.mstart[gid];
-        for (int v = 0; v <= n; ++v, ++q) {
-          const int32_t id = v == 0 ? l : W.members[s0 + v - 1];
+    // producer warp: item headers, member ids and their norms are loaded by the
+    // whole warp one item ahead, so the copy issue never waits on them
+    struct Item {
+      int32_t gid, n, id;  // id / inv: lane k holds vector k of the item (k <= 31)
+      float inv, home;
+      bool valid;
+    };
+    auto load_item = [&](int it) {
+      Item x;
+      x.valid = it < n_items;
+      x.gid = 0;
+      x.n = 0;
+      x.id = 0;
+      x.inv = 0.f;
+      x.home = 0.f;
+      if (!x.valid) return x;
+      const bool is_v = it & 1;
+      const float* norm = is_v ? vnorm : knorm;
+      x.gid = W.list[it >> 1];
+      x.n = W.mcnt[x.gid];
+      const int64_t gb = (x.gid / g.NB) * g.NB;
+      const int s0 = W.mstart[x.gid];
+      x.home = (is_v ? ovnorm : oknorm)[x.gid];
+      if (lane <= x.n) {
+        x.id = lane == 0 ? (int32_t)(x.gid - gb) : W.members[s0 + lane - 1];
+        const float nv = norm[gb + x.id];
+        x.inv = nv > 0.f ? 1.f / nv : 0.f;
+      }
+      return x;
+    };
+    uint32_t q = 0;
+    int it = blockIdx.x;
+    Item cur = load_item(it);
+    while (cur.valid) {
+      const Item nxt = load_item(it + gridDim.x);
+      const bool is_v = it & 1;
+      const T* pool = is_v ? pool_v : pool_k;
+      const int64_t u = cur.gid / g.NB;
+      const int64_t gb = u * g.NB;
+      const int s0 = W.mstart[cur.gid];
+      for (int v = 0; v <= cur.n; ++v, ++q) {
+        int32_t id;
+        float inv;
+        if (v < 32) {
+          id = __shfl_sync(0xffffffffu, cur.id, v);
+          inv = __shfl_sync(0xffffffffu, cur.inv, v);
+        } else {  // large groups: beyond the warp-wide prefetch
+          id = W.members[s0 + v - 1];
+          const float nv = (is_v ? vnorm : knorm)[gb + id];
+          inv = nv > 0.f ? 1.f / nv : 0.f;
+        }
+        if (lane == 0) {
           const int s = q % nbuf;
           mbar_wait(&empty[s], ((q / nbuf) & 1) ^ 1);
-          mbar_expect_tx(&full[s], vbytes);
+          SlotMeta mt;
+          mt.inv = inv;
+          mt.home = cur.home;
+          mt.gid = cur.gid;
+          mt.flags = (v == cur.n ? 1 : 0) | (is_v ? 2 : 0);
+          meta[s] = mt;
+          mbar_expect_tx(&full[s], vbytes);  // release: meta visible after the wait
           const T* src = pool + g.base(u, id);
           uint8_t* dst = ring + (size_t)s * slot_bytes;
           if (!g.head_mode) {
@@ -294,32 +351,24 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
           }
         }
       }
+      cur = nxt;
+      it += gridDim.x;
     }
     return;
   }
-  // consumers
+  // consumers: everything per vector comes from the slot (data + meta)
   const int ct = threadIdx.x - 32;
   const int64_t nch = r / VEC;
   uint32_t q = 0;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
-    const int64_t gid = W.list[it >> 1];
-    const bool is_v = it & 1;
-    T* pool = is_v ? pool_v : pool_k;
-    float* norm = is_v ? vnorm : knorm;
-    const float* onorm = is_v ? ovnorm : oknorm;
-    const int64_t u = gid / g.NB;
-    const int64_t gb = u * g.NB;
-    const int32_t l = (int32_t)(gid % g.NB);
-    const int n = W.mcnt[gid], s0 = W.mstart[gid];
-    float acc[EPT];
+  float acc[EPT];
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) acc[e] = 0.f;
-    for (int v = 0; v <= n; ++v, ++q) {
-      const int32_t id = v == 0 ? l : W.members[s0 + v - 1];
-      const float nv = norm[gb + id];
-      const float inv = nv > 0.f ? 1.f / nv : 0.f;
+  for (int e = 0; e < EPT; ++e) acc[e] = 0.f;
+  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    SlotMeta mt;
+    for (;;) {
       const int s = q % nbuf;
       mbar_wait(&full[s], (q / nbuf) & 1);
+      mt = meta[s];
       const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * slot_bytes);
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
@@ -328,18 +377,24 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
           float x[VEC];
           VecIO<T, VEC>::load(sp + c * VEC, x);
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[k * VEC + e] = fmaf(x[e], inv, acc[k * VEC + e]);
+          for (int e = 0; e < VEC; ++e) acc[k * VEC + e] = fmaf(x[e], mt.inv, acc[k * VEC + e]);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      ++q;
+      if (mt.flags & 1) break;
     }
+    const bool is_v = mt.flags & 2;
+    T* pool = is_v ? pool_v : pool_k;
+    float* norm = is_v ? vnorm : knorm;
+    const int64_t u = mt.gid / g.NB;
+    const int32_t l = (int32_t)(mt.gid % g.NB);
     float ss = 0.f;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) ss = fmaf(acc[e], acc[e], ss);
     const float nrm = sqrtf(consumer_sum(ss, red));
-    const float home = onorm[gid];
-    const float sc = nrm > 0.f ? (home > 0.f ? home : 1.f) / nrm : 0.f;
+    const float sc = nrm > 0.f ? (mt.home > 0.f ? mt.home : 1.f) / nrm : 0.f;
     T* xl = pool + g.base(u, l);
     float rs = 0.f;
 #pragma unroll
@@ -354,8 +409,10 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
         for (int e = 0; e < VEC; ++e) rs = fmaf(rd[e], rd[e], rs);
       }
     }
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) acc[e] = 0.f;
     const float nn = sqrtf(consumer_sum(rs, red));
-    if (ct == 0) norm[gid] = nn;
+    if (ct == 0) norm[mt.gid] = nn;
   }
 }
 
@@ -456,7 +513,7 @@ template <typename T, int EPT>
 cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
                       const void* ovn, int32_t* ws, int64_t n_total, int nbuf, int slot_bytes,
                       cudaStream_t s) {
-  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + 64;
+  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + MG_MAX_BUF * (int)sizeof(SlotMeta) + 64;
   static int attr = 0;  // per instantiation
   if (attr < smem) {
     cudaError_t e = cudaFuncSetAttribute(merge_tma_kernel<T, EPT>,
