@@ -72,10 +72,26 @@ class PagedKvCache:
     mirrored to the GPU (``keys_dev`` / ``values_dev``); torch CUDA tensors
     (float64 / float32 / bfloat16) are used in place without a host copy.
     NaN / Inf entries raise InvalidCacheError (checked on the device).
+
+    ``defer_upload=True`` with host (ideally pinned) torch tensors keeps the
+    cache on the host: fuse_batch / fuse_chunks then stream it to the GPU in
+    layer chunks overlapped with fusion, validating each chunk on the device
+    (a non-finite entry raises InvalidCacheError from the fuse call).
     """
 
-    def __init__(self, dims: CacheDims, keys, values):
+    def __init__(self, dims: CacheDims, keys, values, *, defer_upload: bool = False):
         self.dims = dims
+        self.keys_dev = self.values_dev = None
+        if (defer_upload and isinstance(keys, torch.Tensor) and isinstance(values, torch.Tensor)
+                and not keys.is_cuda and not values.is_cuda):
+            if tuple(keys.shape) != dims.shape or tuple(values.shape) != dims.shape:
+                raise InvalidCacheError(f"keys / values shapes do not match dims {dims.shape}")
+            if keys.dtype != values.dtype or keys.dtype not in (torch.float32, torch.bfloat16):
+                raise InvalidCacheError("deferred upload takes float32 or bfloat16 host tensors")
+            self.keys = keys.contiguous()
+            self.values = values.contiguous()
+            self._device = default_device()
+            return
         if isinstance(keys, torch.Tensor) or isinstance(values, torch.Tensor):
             if not (isinstance(keys, torch.Tensor) and isinstance(values, torch.Tensor)):
                 raise InvalidCacheError("keys and values must both be torch tensors or arrays")
@@ -110,14 +126,20 @@ class PagedKvCache:
             raise InvalidCacheError("cache contains NaN or Inf entries")
         self.keys_dev = kd
         self.values_dev = vd
+        self._device = kd.device
+
+    @property
+    def host_resident(self) -> bool:
+        """True while a deferred-upload cache has not been copied to the GPU."""
+        return self.keys_dev is None
 
     @property
     def dtype(self) -> torch.dtype:
-        return self.keys_dev.dtype
+        return self.keys.dtype if self.keys_dev is None else self.keys_dev.dtype
 
     @property
     def device(self) -> torch.device:
-        return self.keys_dev.device
+        return self._device
 
     def geometry(self, head_mode: int = 0) -> Geometry:
         d = self.dims
@@ -438,11 +460,19 @@ class FusedLayer:
     x / |x|) as float64 numpy; ``directions_device`` keeps it on the GPU.
     """
 
-    def __init__(self, phys_ids: tuple[int, ...], loader=None, directions=None):
-        self.phys_ids = tuple(int(i) for i in phys_ids)
+    def __init__(self, phys_ids, loader=None, directions=None):
+        # phys_ids: a sequence, or a device int32 tensor materialised on access
+        self._ids = phys_ids
         self._loader = loader
         self._dirs = directions
         self._dirs_dev = None
+
+    @property
+    def phys_ids(self) -> tuple[int, ...]:
+        if not isinstance(self._ids, tuple):
+            src = self._ids.cpu().tolist() if isinstance(self._ids, torch.Tensor) else self._ids
+            self._ids = tuple(int(i) for i in src)
+        return self._ids
 
     @property
     def directions_device(self) -> torch.Tensor:

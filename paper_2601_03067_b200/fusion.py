@@ -37,7 +37,7 @@ from .core import (
     default_device,
 )
 from .engine import NONE, FusionEngine, FusionState, Geometry, acc_dtype, dtype_code
-from .errors import ConfigError, InsufficientDataError
+from .errors import ConfigError, InsufficientDataError, InvalidCacheError
 from .schedule import Plan, bff_plan, cff_plan, single_tree_plan
 
 SAMPLES_AUTO_LIMIT = 1 << 22  # pairs across all units and levels
@@ -429,7 +429,7 @@ class _UnitLazy:
 
 def _outcomes_from_state(st: FusionState, keep_samples: bool, rows: int, bpr: int,
                          block_shape: tuple[int, int, int], tables: list[BlockTable] | None = None,
-                         layer_override: int | None = None) -> list[FusionOutcome]:
+                         layer_override: int | None = None, layer_offset: int = 0) -> list[FusionOutcome]:
     run = _RunHost(st, keep_samples)
     run.fetch()
     g = st.geom
@@ -440,11 +440,12 @@ def _outcomes_from_state(st: FusionState, keep_samples: bool, rows: int, bpr: in
     ovnorm = st.orig_vnorm.cpu().numpy().astype(acc_np)
     live_ids_all = st.live_ids
     for u in range(g.units):
-        layer = (u // g.h if g.head_mode else u) if layer_override is None else layer_override
+        layer = ((u // g.h if g.head_mode else u) + layer_offset
+                 if layer_override is None else layer_override)
         head = (u % g.h) if g.head_mode else None
         n_live = int(run.live_count[u])
         ids_dev = live_ids_all[u, :n_live]
-        phys = tuple(ids_dev.cpu().tolist())
+        phys = ids_dev  # ascending live ids, materialised on access
 
         def loader(pool, norms, ids=ids_dev, u=u):
             out = torch.empty((ids.numel(), g.r), dtype=acc_dtype(pool.dtype), device=pool.device)
@@ -503,6 +504,70 @@ def _head_mode(cfg: FusionConfig) -> int:
     return 1 if cfg.head_mode == "per_head" else 0
 
 
+STREAM_LAYERS = 4  # layers per H2D chunk when streaming a host-resident cache
+
+
+def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_place: bool,
+                keep_samples: bool, path: int) -> list[tuple[FusionState, int]]:
+    """Fuse every unit of the cache; returns (state, first layer) per engine run.
+
+    Device-resident caches run as one engine pass. Host-resident caches
+    (PagedKvCache(..., defer_upload=True)) stream to the GPU in chunks of
+    STREAM_LAYERS layers on a copy stream while earlier chunks fuse on the
+    current stream; every chunk is validated for NaN / Inf on the device.
+    """
+    if not cache.host_resident:
+        geom = cache.geometry(hm)
+        pk, pv = _pools(cache, in_place)
+        engine = FusionEngine(geom, plan, pk.dtype, pk.device, path)
+        return [(engine.run(pk.reshape(-1), pv.reshape(-1), threshold, keep_samples=keep_samples), 0)]
+    d = cache.dims
+    dev = cache.device
+    kd = torch.empty(d.shape, dtype=cache.dtype, device=dev)
+    vd = torch.empty(d.shape, dtype=cache.dtype, device=dev)
+    compute = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    copy.wait_stream(compute)  # kd / vd allocated on the compute stream
+    chunks = [(c0, min(d.L, c0 + STREAM_LAYERS)) for c0 in range(0, d.L, STREAM_LAYERS)]
+    ready = []
+    with torch.cuda.stream(copy):
+        for c0, c1 in chunks:
+            kd[c0:c1].copy_(cache.keys[c0:c1], non_blocking=True)
+            vd[c0:c1].copy_(cache.values[c0:c1], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            ready.append(ev)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    engines: dict[int, FusionEngine] = {}
+    out = []
+    dt = dtype_code(cache.dtype)
+    for (c0, c1), ev in zip(chunks, ready):
+        compute.wait_event(ev)
+        kc, vc = kd[c0:c1], vd[c0:c1]
+        N.call("kvf_count_nonfinite", N.ptr(kc), dt, kc.numel(), N.ptr(bad), N.stream_ptr())
+        N.call("kvf_count_nonfinite", N.ptr(vc), dt, vc.numel(), N.ptr(bad), N.stream_ptr())
+        nl = c1 - c0
+        if nl not in engines:
+            engines[nl] = FusionEngine(Geometry(nl, d.B * d.p, d.t, d.h, d.d, hm), plan, cache.dtype,
+                                       dev, path)
+        st = engines[nl].run(kc.reshape(-1), vc.reshape(-1), threshold, keep_samples=keep_samples)
+        out.append((st, c0))
+    kd.record_stream(copy)
+    vd.record_stream(copy)
+    if int(bad.item()):
+        raise InvalidCacheError("cache contains NaN or Inf entries")
+    if in_place:
+        cache.keys_dev, cache.values_dev = kd, vd
+    return out
+
+
+def _outcomes(runs, keep_samples, rows, bpr, shape) -> list[FusionOutcome]:
+    outs: list[FusionOutcome] = []
+    for st, c0 in runs:
+        outs.extend(_outcomes_from_state(st, keep_samples, rows, bpr, shape, layer_offset=c0))
+    return outs
+
+
 def fuse_batch(cache: PagedKvCache, cfg: FusionConfig, *, in_place: bool = False,
                keep_samples: bool | None = None, path: int = N.PATH_AUTO) -> list[FusionOutcome]:
     """Batch Fast-Fusion across requests, all layers at once (fusion.py:360-374).
@@ -516,12 +581,10 @@ def fuse_batch(cache: PagedKvCache, cfg: FusionConfig, *, in_place: bool = False
     hm = _head_mode(cfg)
     geom = cache.geometry(hm)
     plan = bff_plan(dims.B, dims.p, cfg.group_size)
-    pk, pv = _pools(cache, in_place)
-    engine = FusionEngine(geom, plan, pk.dtype, pk.device, path)
     ks = _want_samples(keep_samples, plan, geom.units)
-    st = engine.run(pk.reshape(-1), pv.reshape(-1), cfg.threshold, keep_samples=ks)
+    runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path)
     shape = (dims.t, 1, dims.d) if hm else (dims.t, dims.h, dims.d)
-    return _outcomes_from_state(st, ks, dims.B, dims.p, shape)
+    return _outcomes(runs, ks, dims.B, dims.p, shape)
 
 
 def fuse_chunks(cache: PagedKvCache, cfg: FusionConfig, chunk_tokens: int, *,
@@ -539,15 +602,13 @@ def fuse_chunks(cache: PagedKvCache, cfg: FusionConfig, chunk_tokens: int, *,
     hm = _head_mode(cfg)
     geom = cache.geometry(hm)
     plan = cff_plan(dims.B, C, bpc, cfg.group_size)
-    pk, pv = _pools(cache, in_place)
-    engine = FusionEngine(geom, plan, pk.dtype, pk.device, path)
     ks = _want_samples(keep_samples, plan, geom.units)
-    st = engine.run(pk.reshape(-1), pv.reshape(-1), cfg.threshold, keep_samples=ks)
+    runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path)
     shape = (dims.t, 1, dims.d) if hm else (dims.t, dims.h, dims.d)
-    outcomes = _outcomes_from_state(st, ks, dims.B * C, bpc, shape)
-    ref = st.refcount.cpu().numpy()
-    for u, oc in enumerate(outcomes):
-        oc.fused.table.reusable = set(int(p) for p in np.nonzero(ref[u] > 1)[0])
+    outcomes = _outcomes(runs, ks, dims.B * C, bpc, shape)
+    for oc in outcomes:  # reusable = {refcount > 1} (fusion.py:409-411)
+        ref = oc.fused.table.device_refcount.cpu().numpy()
+        oc.fused.table.reusable = set(int(p) for p in np.nonzero(ref > 1)[0])
     return outcomes
 
 
