@@ -25,6 +25,9 @@ def grouped(indices: list[int], group_size: int | None) -> list[list[int]]:
     return [list(indices[i : i + group_size]) for i in range(0, len(indices), group_size)]
 
 
+TILE_BAND = 4  # tile rows per launch-order band (L2 reuse of operand tiles)
+
+
 @dataclass(frozen=True)
 class MergeNode:
     height: int
@@ -56,14 +59,20 @@ class Level:
     row_merge: np.ndarray  # int32 [rows], merge index of the row at this level or -1
     tiles: dict = field(default_factory=dict)  # (tm, tn) -> (tiles [nt,3], tile_off [nm+1])
 
-    def tiling(self, tm: int, tn: int) -> tuple[np.ndarray, np.ndarray]:
-        key = (tm, tn)
+    def tiling(self, tm: int, tn: int, band: int = TILE_BAND) -> tuple[np.ndarray, np.ndarray]:
+        """Tiles (merge, i0, j0) of every merge, launch-ordered in bands of
+        `band` tile rows walked column by column, so CTAs running together
+        share A and B operand rows in L2."""
+        key = (tm, tn, band)
         if key not in self.tiles:
             tl, off = [], [0]
             for m, (lb, mid, re) in enumerate(self.merges.tolist()):
-                for i0 in range(0, mid - lb, tm):
-                    for j0 in range(0, re - mid, tn):
-                        tl.append((m, i0, j0))
+                rows = list(range(0, mid - lb, tm))
+                cols = list(range(0, re - mid, tn))
+                for b0 in range(0, len(rows), band):
+                    for j0 in cols:
+                        for i0 in rows[b0 : b0 + band]:
+                            tl.append((m, i0, j0))
                 off.append(len(tl))
             self.tiles[key] = (
                 np.asarray(tl, dtype=np.int32).reshape(-1, 3),
