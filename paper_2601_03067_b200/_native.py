@@ -7,12 +7,15 @@ If it is missing, `lib()` raises immediately.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 from .errors import AlignmentError, ConfigError, CorruptionError, KvFuseError
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libkvfuse_b200.so"
+LIB_PATH = Path(
+    os.environ.get("KVF_LIB") or Path(__file__).resolve().parent / "_lib" / "libkvfuse_b200.so"
+)  # KVF_LIB: load another build of the library (A/B measurements)
 
 KVF_OK = 0
 KVF_ERR_INVALID = 1

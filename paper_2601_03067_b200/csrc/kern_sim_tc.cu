@@ -14,8 +14,8 @@
 //   warp 1      MMA issuer (leader): 4 x tcgen05.mma.cta_group::2.kind::f16
 //               per 64-wide k-step; tcgen05.commit multicasts the stage
 //               release to both CTAs
-//   warp 2      TMEM allocator (256 columns, cta_group::2)
-//   warps 3-7   column metadata; warps 4..7 epilogue: tcgen05.ld 32x32b.x32
+//   warp 2      TMEM allocator (2 x 256 columns, cta_group::2)
+//   warps 4..7  epilogue: per-tile column metadata, tcgen05.ld 32x32b.x32
 //               -> sim = acc / (|x_i||x_j|), alive/fusable masks, strict
 //               '> thr' (pairs within resc_band deferred to the exact
 //               re-score), per-column min row via redux.sync + smem atomicMin
@@ -24,7 +24,9 @@
 // the epilogue, so level-1 similarities are exact-input bf16 products.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <mutex>
+#include <unordered_map>
 #include "kernels.h"
 
 namespace kvf {
@@ -38,7 +40,7 @@ constexpr int STAGES = 6;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BNH * BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;  // two 256-column accumulators
 constexpr int NTHREADS = 256;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*meta*/;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // cluster smem address of CTA 0
@@ -129,8 +131,76 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 }  // namespace
 
+struct TileInfo {
+  bool active;
+  int64_t ul, u;
+  int m, i0, j0, lb, mid, re, pl, pm, pr;
+};
+
+// Work item w (unit-major: clusters running together share a unit's operand
+// rows in L2) -> tile geometry.
+__device__ __forceinline__ TileInfo tile_info(int w, int nt, int64_t u0, const Geom& g,
+                                              const int32_t* __restrict__ merges,
+                                              const int32_t* __restrict__ tiles,
+                                              const int32_t* __restrict__ rank, bool staged) {
+  TileInfo t;
+  t.ul = w / nt;
+  const int tile = w - (int)t.ul * nt;
+  t.u = u0 + t.ul;
+  t.m = tiles[3 * tile];
+  t.i0 = tiles[3 * tile + 1];
+  t.j0 = tiles[3 * tile + 2];
+  t.lb = merges[3 * t.m];
+  t.mid = merges[3 * t.m + 1];
+  t.re = merges[3 * t.m + 2];
+  t.pl = t.lb;
+  t.pm = t.mid;
+  t.pr = t.re;
+  if (staged) {  // compacted mode: rows are positions in the unit's alive list
+    const int32_t* rk = rank + t.u * (g.NB + 1);
+    t.pl = rk[t.lb];
+    t.pm = rk[t.mid];
+    t.pr = rk[t.re];
+  }
+  t.active = t.i0 < t.pm - t.pl && t.j0 < t.pr - t.pm;
+  return t;
+}
+
+__device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                   cluster_addr(bar, cta))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void st_cluster_s32(const void* p, uint32_t cta, int32_t v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(cluster_addr(p, cta)), "r"(v) : "memory");
+}
+
+constexpr int SCHED_DEPTH = 4;
+// sched_empty arrivals per slot: leader MMA warp + peer producer + 4 epilogue
+// warps in each CTA
+constexpr uint32_t kSchedConsumers = 10;
+
+// Persistent: P CTA pairs pull work items from a global counter (the leader's
+// producer thread fetches, skips tiles beyond the alive blocks, and broadcasts
+// the item to both CTAs' roles through a 4-deep shared-memory ring). TMEM
+// holds two 256-column accumulators, so the epilogue of tile k overlaps the
+// MMAs of tile k + 1 (tmem_full / tmem_empty barrier pair per buffer).
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
-sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
+sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int64_t nU,
               const float* __restrict__ knorm, const uint8_t* __restrict__ fusable,
               const uint8_t* __restrict__ alive, int32_t* __restrict__ absorber,
               const int32_t* __restrict__ merges, const int32_t* __restrict__ tiles, int nt,
@@ -138,67 +208,47 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
               const int64_t* __restrict__ sample_off, int64_t sample_stride,
               const int32_t* __restrict__ live, const int32_t* __restrict__ rank,
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
-              float resc_band) {
+              float resc_band, int32_t* __restrict__ work_counter) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* meta = smem + STAGES * STAGE_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta);
   uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tmem_full = empty_bar + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
-  float* inv_j = reinterpret_cast<float*>(meta + 256);
-  int32_t* colmin = reinterpret_cast<int32_t*>(meta + 256 + 4 * BN);
-  uint8_t* ok_j = meta + 256 + 8 * BN;
-  double* red = reinterpret_cast<double*>(meta + 256 + 9 * BN);            // 4 warps x 5
-  int32_t* colid = reinterpret_cast<int32_t*>(meta + 256 + 9 * BN + 256);  // block ids
+  uint64_t* tmem_full = empty_bar + STAGES;           // [2]
+  uint64_t* tmem_empty = tmem_full + 2;               // [2], used on the leader
+  uint64_t* sched_full = tmem_empty + 2;              // [SCHED_DEPTH]
+  uint64_t* sched_empty = sched_full + SCHED_DEPTH;   // [SCHED_DEPTH], used on the leader
+  int32_t* sched_w = reinterpret_cast<int32_t*>(sched_empty + SCHED_DEPTH);  // [SCHED_DEPTH]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_w + SCHED_DEPTH);
+  float* inv_j = reinterpret_cast<float*>(meta + 512);
+  int32_t* colmin = reinterpret_cast<int32_t*>(meta + 512 + 4 * BN);
+  uint8_t* ok_j = meta + 512 + 8 * BN;
+  double* red = reinterpret_cast<double*>(meta + 512 + 9 * BN);            // 4 warps x 5
+  int32_t* colid = reinterpret_cast<int32_t*>(meta + 512 + 9 * BN + 256);  // block ids
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
   const bool leader = crank == 0;
-  const int tile = blockIdx.x >> 1;
-  const int slot = blockIdx.x;  // partials slot (2 per tile)
-  const int64_t ul = blockIdx.y, u = u0 + ul;
-  const int64_t gb = u * g.NB;
-  const int m = tiles[3 * tile], i0 = tiles[3 * tile + 1], j0 = tiles[3 * tile + 2];
-  const int lb = merges[3 * m], mid = merges[3 * m + 1], re = merges[3 * m + 2];
-  // compacted mode: rows are positions in the unit's ascending alive list and
-  // the operands come from the staged (compacted) copy of the alive K rows
   const bool staged = live != nullptr;
-  int pl = lb, pm = mid, pr = re;
-  if (staged) {
-    const int32_t* rk = rank + u * (g.NB + 1);
-    pl = rk[lb];
-    pm = rk[mid];
-    pr = rk[re];
-  }
-  const int left_n = pm - pl, right_n = pr - pm;
-  if (i0 >= left_n || j0 >= right_n) {  // tile fully beyond the alive blocks (both CTAs)
-    if (threadIdx.x == 0) {
-      double* pp = partials + ((int64_t)ul * gridDim.x + slot) * 5;
-      pp[0] = pp[1] = pp[2] = 0.0;
-      pp[3] = INFINITY;
-      pp[4] = -INFINITY;
-    }
-    return;
-  }
-  const int mi0 = i0 + (int)crank * BM;          // this CTA's first A row in the merge
-  const int ni = max(0, min(BM, left_n - mi0));  // valid rows of this CTA
-  const int nj = min(BN, right_n - j0);
-  const int layer = g.head_mode ? (int)(u / g.h) : (int)u;
-  const int head = g.head_mode ? (int)(u % g.h) : 0;
+  const int nwork = (int)(nt * nU);
+  const int P = (int)(gridDim.x >> 1);
+  const int layer_div = g.head_mode ? g.h : 1;
   const int dpc = g.d / BK;
   const int nk = g.head_mode ? g.t * dpc : g.t * g.h * dpc;
-  const int rowA = staged ? (int)(ul * g.NB) + pl + mi0 : (int)(layer * g.NB) + lb + mi0;
-  const int rowB = (staged ? (int)(ul * g.NB) + pm + j0 : (int)(layer * g.NB) + mid + j0) +
-                   (int)crank * BNH;
-  const int32_t* lv = live + gb;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tmem_full[b], 1);
+      mbar_init(&tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    for (int b = 0; b < SCHED_DEPTH; ++b) {
+      mbar_init(&sched_full[b], 1);
+      mbar_init(&sched_empty[b], kSchedConsumers);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -206,17 +256,6 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-  }
-  if (warp >= 3) {  // column metadata (160 threads cover 256 columns)
-    for (int c = threadIdx.x - 96; c < BN; c += NTHREADS - 96) {
-      const int64_t bj = gb + (c < nj ? (staged ? lv[pm + j0 + c] : mid + j0 + c) : 0);
-      const bool ok = c < nj && alive[bj] && fusable[bj];
-      colid[c] = (int32_t)(bj - gb);
-      const float nv = ok ? knorm[bj] : 0.f;
-      ok_j[c] = ok;
-      inv_j[c] = nv > 0.f ? 1.f / nv : 0.f;
-      colmin[c] = kNone;
-    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   cluster_sync();  // barriers of both CTAs initialised, TMEM allocated
@@ -226,127 +265,218 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0,
   if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-      for (int ks = 0; ks < nk; ++ks) {
-        const int s = ks % STAGES;
-        const uint32_t ph = (ks / STAGES) & 1;
-        mbar_wait(&empty_bar[s], ph ^ 1);
-        const int dc = ks % dpc;
-        const int rest = ks / dpc;
-        const int hh = g.head_mode ? head : rest % g.h;
-        const int tok = g.head_mode ? rest : rest / g.h;
-        // pool map: (d, h, t, rows); staged map: (64, r/64, 1, rows)
-        const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        uint8_t* sb = sa + A_BYTES;
-        if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
-        tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
-        tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
+      uint32_t kk = 0;  // global k-step counter (ring position)
+      for (uint32_t it = 0;; ++it) {
+        const int sl = it % SCHED_DEPTH;
+        const uint32_t sph = (it / SCHED_DEPTH) & 1;
+        int w;
+        TileInfo t;
+        if (leader) {  // fetch the next tile with alive blocks; publish it to both CTAs
+          mbar_wait_cluster(&sched_empty[sl], sph ^ 1);
+          for (;;) {
+            w = atomicAdd(work_counter, 1);
+            if (w >= nwork) {
+              if (w == nwork + P - 1) atomicExch(work_counter, 0);  // last fetch of the launch
+              w = -1;
+              break;
+            }
+            t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+            if (t.active) break;
+            const int tile = w - (int)t.ul * nt;  // tile fully beyond the alive blocks
+            double* pp = partials + ((int64_t)t.ul * 2 * nt + 2 * tile) * 5;
+            for (int q = 0; q < 2; ++q) {
+              pp[5 * q + 0] = pp[5 * q + 1] = pp[5 * q + 2] = 0.0;
+              pp[5 * q + 3] = INFINITY;
+              pp[5 * q + 4] = -INFINITY;
+            }
+          }
+          sched_w[sl] = w;
+          st_cluster_s32(&sched_w[sl], 1, w);
+          mbar_arrive_cluster(&sched_full[sl], 0);
+          mbar_arrive_cluster(&sched_full[sl], 1);
+        } else {
+          mbar_wait_cluster(&sched_full[sl], sph);
+          w = sched_w[sl];
+          mbar_arrive_cluster(&sched_empty[sl], 0);
+          if (w >= 0) t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+        }
+        if (w < 0) break;
+        const int layer = (int)(t.u / layer_div);
+        const int head = g.head_mode ? (int)(t.u % g.h) : 0;
+        const int mi0 = t.i0 + (int)crank * BM;
+        const int rowA = staged ? (int)(t.ul * g.NB) + t.pl + mi0 : layer * g.NB + t.lb + mi0;
+        const int rowB =
+            (staged ? (int)(t.ul * g.NB) + t.pm + t.j0 : layer * g.NB + t.mid + t.j0) +
+            (int)crank * BNH;
+        for (int ks = 0; ks < nk; ++ks, ++kk) {
+          const int s = kk % STAGES;
+          const uint32_t ph = (kk / STAGES) & 1;
+          mbar_wait(&empty_bar[s], ph ^ 1);
+          const int dc = ks % dpc;
+          const int rest = ks / dpc;
+          const int hh = g.head_mode ? head : rest % g.h;
+          const int tok = g.head_mode ? rest : rest / g.h;
+          // pool map: (d, h, t, rows); staged map: (64, r/64, 1, rows)
+          const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+          tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
+          tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
+        }
       }
     }
   } else if (warp == 1) {
     if (leader && lane == 0) {
-      for (int ks = 0; ks < nk; ++ks) {
-        const int s = ks % STAGES;
-        const uint32_t ph = (ks / STAGES) & 1;
-        mbar_wait(&full_bar[s], ph);
+      uint32_t kk = 0, tc = 0;
+      for (uint32_t it = 0;; ++it) {
+        const int sl = it % SCHED_DEPTH;
+        mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
+        const int w = sched_w[sl];
+        mbar_arrive_cluster(&sched_empty[sl], 0);
+        if (w < 0) break;
+        const uint32_t acc = tc & 1;
+        mbar_wait_cluster(&tmem_empty[acc], ((tc >> 1) & 1) ^ 1);  // epilogue drained it
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-        const uint32_t sb = sa + A_BYTES;
+        const uint32_t dst = tmem_base + acc * BN;
+        for (int ks = 0; ks < nk; ++ks, ++kk) {
+          const int s = kk % STAGES;
+          const uint32_t ph = (kk / STAGES) & 1;
+          mbar_wait(&full_bar[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
+          const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          umma_bf16_2sm(tmem_base, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32),
-                        (ks | k) != 0);
-        umma_commit_2sm(&empty_bar[s]);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_2sm(dst, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), (ks | k) != 0);
+          umma_commit_2sm(&empty_bar[s]);
+        }
+        umma_commit_2sm(&tmem_full[acc]);
+        ++tc;
       }
-      umma_commit_2sm(tmem_full);
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
     const int row = ew * 32 + lane;
-    const int32_t my_id = row < ni ? (staged ? lv[pl + mi0 + row] : lb + mi0 + row) : 0;
-    const int64_t bi = gb + my_id;
-    const bool ok_i = row < ni && alive[bi] && fusable[bi];
-    const float ni_v = ok_i ? knorm[bi] : 0.f;
-    const float inv_i = ni_v > 0.f ? 1.f / ni_v : 0.f;
-    float cnt = 0.f, s1 = 0.f, s2 = 0.f, mn = INFINITY, mx = -INFINITY;
-    double* samp = samples ? samples + ul * sample_stride + sample_off[m] : nullptr;
+    const int et = threadIdx.x - 128;
+    uint32_t tc = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int sl = it % SCHED_DEPTH;
+      mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
+      const int w = sched_w[sl];
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
+      if (w < 0) break;
+      const TileInfo t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+      const int tile = w - (int)t.ul * nt;
+      double* pp = partials + ((int64_t)t.ul * 2 * nt + 2 * tile + crank) * 5;
+      const int64_t gb = t.u * g.NB;
+      const int32_t* lv = live + gb;
+      const int mi0 = t.i0 + (int)crank * BM;
+      const int ni = max(0, min(BM, t.pm - t.pl - mi0));  // valid rows of this CTA
+      const int nj = min(BN, t.pr - t.pm - t.j0);
+      for (int c = et; c < BN; c += 128) {  // column metadata
+        const int64_t bj = gb + (c < nj ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
+        const bool ok = c < nj && alive[bj] && fusable[bj];
+        colid[c] = (int32_t)(bj - gb);
+        const float nv = ok ? knorm[bj] : 0.f;
+        ok_j[c] = ok;
+        inv_j[c] = nv > 0.f ? 1.f / nv : 0.f;
+        colmin[c] = kNone;
+      }
+      const int32_t my_id = row < ni ? (staged ? lv[t.pl + mi0 + row] : t.lb + mi0 + row) : 0;
+      const int64_t bi = gb + my_id;
+      const bool ok_i = row < ni && alive[bi] && fusable[bi];
+      const float ni_v = ok_i ? knorm[bi] : 0.f;
+      const float inv_i = ni_v > 0.f ? 1.f / ni_v : 0.f;
+      float cnt = 0.f, s1 = 0.f, s2 = 0.f, mn = INFINITY, mx = -INFINITY;
+      double* samp = samples ? samples + t.ul * sample_stride + sample_off[t.m] : nullptr;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // column metadata visible
 
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + c0, v);
-      int32_t mine = kNone;
+      const uint32_t acc = tc & 1;
+      mbar_wait(&tmem_full[acc], (tc >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, v);
+        int32_t mine = kNone;
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const int col = c0 + c;
-        const bool ok = ok_i && ok_j[col];
-        const float s = __uint_as_float(v[c]) * inv_i * inv_j[col];
-        int32_t cand = kNone;
-        if (ok) {
-          cnt += 1.f;
-          s1 += s;
-          s2 += s * s;
-          mn = fminf(mn, s);
-          mx = fmaxf(mx, s);
-          // The tensor-core fp32 accumulation over r/16 steps can be off by
-          // ~1e-4 relative: pairs that close to the threshold are deferred to
-          // an exact float64 re-score (kvf_rescore) instead of decided here.
-          bool decided = true;
-          if (resc != nullptr && fabsf(s - thr) <= resc_band) {
-            const int pos = atomicAdd(resc_count, 1);
-            if (pos < resc_cap) {
-              int4 e;
-              e.x = (int)u;
-              e.y = my_id;
-              e.z = colid[col];
-              e.w = m;
-              reinterpret_cast<int4*>(resc)[pos] = e;
-              decided = false;
+        for (int c = 0; c < 32; ++c) {
+          const int col = c0 + c;
+          const bool ok = ok_i && ok_j[col];
+          const float s = __uint_as_float(v[c]) * inv_i * inv_j[col];
+          int32_t cand = kNone;
+          if (ok) {
+            cnt += 1.f;
+            s1 += s;
+            s2 += s * s;
+            mn = fminf(mn, s);
+            mx = fmaxf(mx, s);
+            // The tensor-core fp32 accumulation over r/16 steps can be off by
+            // ~1e-4 relative: pairs that close to the threshold are deferred to
+            // an exact float64 re-score (kvf_rescore) instead of decided here.
+            bool decided = true;
+            if (resc != nullptr && fabsf(s - thr) <= resc_band) {
+              const int pos = atomicAdd(resc_count, 1);
+              if (pos < resc_cap) {
+                int4 e;
+                e.x = (int)t.u;
+                e.y = my_id;
+                e.z = colid[col];
+                e.w = t.m;
+                reinterpret_cast<int4*>(resc)[pos] = e;
+                decided = false;
+              }
             }
+            if (decided && s > thr) cand = my_id;
           }
-          if (decided && s > thr) cand = my_id;
+          if (samp && row < ni && col < nj)
+            samp[(int64_t)(my_id - t.lb) * (t.re - t.mid) + (colid[col] - t.mid)] =
+                ok ? (double)s : (double)NAN;
+          const int32_t wmin = (int32_t)__reduce_min_sync(0xffffffffu, (uint32_t)cand);
+          if (lane == c) mine = wmin;
         }
-        if (samp && row < ni && col < nj)
-          samp[(int64_t)(my_id - lb) * (re - mid) + (colid[col] - mid)] = ok ? (double)s : (double)NAN;
-        const int32_t wmin = (int32_t)__reduce_min_sync(0xffffffffu, (uint32_t)cand);
-        if (lane == c) mine = wmin;
+        if (mine != kNone) atomicMin(&colmin[c0 + lane], mine);
       }
-      if (mine != kNone) atomicMin(&colmin[c0 + lane], mine);
-    }
-    // per-CTA similarity moments: deterministic warp tree, then fixed warp order
-    double dc = cnt, d1 = s1, d2 = s2, dmn = mn, dmx = mx;
+      // accumulator drained: hand the buffer back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+      ++tc;
+      // per-CTA similarity moments: deterministic warp tree, then fixed warp order
+      double dc = cnt, d1 = s1, d2 = s2, dmn = mn, dmx = mx;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      dc += __shfl_xor_sync(0xffffffffu, dc, o);
-      d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-      d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-      dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
-      dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
-    }
-    if (lane == 0) {
-      red[ew * 5 + 0] = dc;
-      red[ew * 5 + 1] = d1;
-      red[ew * 5 + 2] = d2;
-      red[ew * 5 + 3] = dmn;
-      red[ew * 5 + 4] = dmx;
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    for (int c = threadIdx.x - 128; c < BN; c += 128) {
-      const int32_t cm = colmin[c];
-      if (cm != kNone) atomicMin(&absorber[gb + colid[c]], cm);
-    }
-    if (threadIdx.x == 128) {
-      double o[5] = {0, 0, 0, INFINITY, -INFINITY};
-      for (int w = 0; w < 4; ++w) {
-        o[0] += red[w * 5 + 0];
-        o[1] += red[w * 5 + 1];
-        o[2] += red[w * 5 + 2];
-        o[3] = fmin(o[3], red[w * 5 + 3]);
-        o[4] = fmax(o[4], red[w * 5 + 4]);
+      for (int o = 16; o > 0; o >>= 1) {
+        dc += __shfl_xor_sync(0xffffffffu, dc, o);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+        d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+        dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
+        dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
       }
-      double* pp = partials + ((int64_t)ul * gridDim.x + slot) * 5;
-      for (int q = 0; q < 5; ++q) pp[q] = o[q];
+      if (lane == 0) {
+        red[ew * 5 + 0] = dc;
+        red[ew * 5 + 1] = d1;
+        red[ew * 5 + 2] = d2;
+        red[ew * 5 + 3] = dmn;
+        red[ew * 5 + 4] = dmx;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      for (int c = et; c < BN; c += 128) {
+        const int32_t cm = colmin[c];
+        if (cm != kNone) atomicMin(&absorber[gb + colid[c]], cm);
+      }
+      if (et == 0) {
+        double o[5] = {0, 0, 0, INFINITY, -INFINITY};
+        for (int q = 0; q < 4; ++q) {
+          o[0] += red[q * 5 + 0];
+          o[1] += red[q * 5 + 1];
+          o[2] += red[q * 5 + 2];
+          o[3] = fmin(o[3], red[q * 5 + 3]);
+          o[4] = fmax(o[4], red[q * 5 + 4]);
+        }
+        for (int q = 0; q < 5; ++q) pp[q] = o[q];
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // metadata free for the next tile
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -375,6 +505,23 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
       fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   });
   return fn;
+}
+// Tile-scheduler counter of the persistent kernel, one per stream (the kernel
+// leaves it at zero when it exits).
+int32_t* work_counter(cudaStream_t s) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, int32_t*> counters;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (reinterpret_cast<uint64_t>(s) << 8) ^ (uint64_t)dev;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = counters.find(key);
+  if (it != counters.end()) return it->second;
+  int32_t* p = nullptr;
+  if (cudaMalloc(&p, sizeof(int32_t)) != cudaSuccess || cudaMemset(p, 0, sizeof(int32_t)) != cudaSuccess)
+    return nullptr;
+  counters.emplace(key, p);
+  return p;
 }
 }  // namespace
 
@@ -446,11 +593,31 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   }
   float thr = (float)a.thr;
   if ((double)thr > a.thr) thr = nextafterf(thr, -INFINITY);  // (float)s > thr_f <=> s > thr
-  dim3 grid(2 * a.nt, (unsigned)a.nU);
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2, 1, 1);
+    cfg.blockDim = dim3(NTHREADS, 1, 1);
+    cfg.dynamicSmemBytes = SMEM_BYTES;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, sim_tc_kernel, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      n = sms / 2;
+    }
+    max_clusters = n;
+  }
+  const int64_t nwork = (int64_t)a.nt * a.nU;
+  if (nwork + max_clusters >= INT32_MAX) return cudaErrorInvalidValue;
+  int32_t* counter = work_counter(s);
+  if (counter == nullptr) return cudaErrorMemoryAllocation;
+  dim3 grid(2 * (unsigned)std::min<int64_t>(nwork, max_clusters), 1);
   sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
-      tmap, g, a.u0, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
+      tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
-      a.resc_count, (int)a.resc_cap, (float)a.resc_band);
+      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter);
   return cudaGetLastError();
 }
 
