@@ -207,6 +207,50 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
                      void* out, void* lse, void* probs, void* workspace,
                      int64_t workspace_bytes, void* stream);
 
+/* Sharing-aware decode schedule (PAPER.md:56, 130-131:
+ * a fused block shared by several requests should be fetched once). For
+ * serving batches it replaces the request-major loop of attention.py:58-80;
+ * results equal kvf_paged_decode up to fp32 summation order (softmax is
+ * permutation invariant). Per layer and head unit hu (nh = h units when
+ * head_mode == 1, else 1), with nit = ceil(p_blocks / item_blocks):
+ *   order int32 [nh][B][p_blocks]  request b's positions sorted by physical
+ *                                  block (-1 past seq_blocks[b])
+ *   meta  int32 [nh][B*nit]        b*nit + k of each item, items ascending by
+ *                                  first physical block; n_items[hu] valid
+ *   phys  int32 [nh][B*nit][item_blocks] physical block of each item slot
+ *                                  (-1 = padding); ks / vs float, same shape:
+ *                                  the slots' K / V scales
+ * item_blocks: 8 or 16 (kvf_decode_schedule_item_blocks() = tuned default).
+ * workspace: kvf_decode_schedule_ws_ints() int32 words. Rebuild the schedule
+ * after any change of the layer's table or scales. */
+int kvf_decode_schedule_item_blocks(void);
+int64_t kvf_decode_schedule_ws_ints(int head_mode, int h, int64_t NB, int64_t B,
+                                    int64_t p_blocks, int item_blocks);
+int kvf_decode_schedule(const int32_t* table, const void* k_scale,
+                        const void* v_scale, int64_t L, int64_t NB, int t,
+                        int h, int d, int head_mode, int64_t layer, int64_t B,
+                        int64_t p_blocks, const int32_t* seq_blocks,
+                        int item_blocks, int32_t* order, int32_t* meta,
+                        int32_t* phys, float* ks, float* vs, int32_t* n_items,
+                        int32_t* workspace, int64_t workspace_ints,
+                        void* stream);
+/* K6 over a schedule: persistent warps sweep the items head by head, so
+ * requests sharing a fused block read it within one L2 window. bf16 pools,
+ * d in {64, 128}, t | 32. Same q / out / lse contract as kvf_paged_decode
+ * (no probability output); workspace >= B*Hq*nit*(d+2)*4 bytes. */
+int kvf_paged_decode_sched(const void* q, int q_dtype, const void* pool_k,
+                           const void* pool_v, int dtype, int64_t L,
+                           int64_t NB, int t, int h, int d, int head_mode,
+                           int64_t layer, const int32_t* table,
+                           const void* k_scale, const void* v_scale, int64_t B,
+                           int64_t p_blocks, const int32_t* seq_blocks, int Hq,
+                           double sm_scale, void* out, void* lse,
+                           int item_blocks, const int32_t* meta,
+                           const int32_t* phys, const float* ks,
+                           const float* vs, const int32_t* n_items,
+                           void* workspace, int64_t workspace_bytes,
+                           void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -8,7 +8,10 @@ behind a C ABI (include/kvfuse_b200.h, libkvfuse_b200.so). See DESIGN.md.
 from .attention import (
     AttentionQuery,
     SoftmaxDistribution,
+    DecodeSchedule,
     attention_drift,
+    decode_schedule,
+    state_decode_schedule,
     paged_attention,
     paged_decode,
     softmax,
@@ -65,7 +68,7 @@ __all__ = [
     "FusionReport", "FusionState", "Geometry", "InsufficientDataError", "InvalidCacheError",
     "KvFuseError", "LayerView", "MergeRecord", "PagedKvCache", "SoftmaxDistribution",
     "UnfoldedLayer", "ZeroVectorError", "adapt_threshold", "attention_drift", "cff_chunk_count",
-    "cosine_similarity", "fast_fusion", "fuse_batch", "fuse_chunks", "paged_attention",
-    "paged_decode", "refold", "reports_to_csv", "softmax", "tune_threshold", "unfold_bff",
+    "DecodeSchedule", "cosine_similarity", "decode_schedule", "fast_fusion", "fuse_batch", "fuse_chunks", "paged_attention",
+    "paged_decode", "refold", "reports_to_csv", "softmax", "state_decode_schedule", "tune_threshold", "unfold_bff",
     "unfold_cff",
 ]

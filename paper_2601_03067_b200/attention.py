@@ -90,17 +90,112 @@ def _decode(q: torch.Tensor, pool_k, pool_v, geom: Geometry, layer: int, table, 
     return out, lse, probs
 
 
+@dataclass
+class DecodeSchedule:
+    """Sharing-aware visit order of one layer's slots (kvf_decode_schedule).
+
+    order[hu, b, :] lists request b's block positions sorted by the physical
+    block they map to (-1 past seq_blocks); the n_items[hu] items -- chunks of
+    `item_blocks` sorted positions of one request -- are ordered by their first
+    physical block: meta[hu, i] = b * nit + k, and phys / ks / vs[hu, i, :]
+    hold the item's physical blocks (-1 = padding) and K / V scales. Softmax
+    is permutation invariant, so decoding in this order gives the
+    request-major result (up to fp32 summation order) while requests sharing
+    a fused block fetch it within one L2 window. Valid
+    until the layer's table or scales change.
+    """
+
+    layer: int
+    B: int
+    p_blocks: int
+    item_blocks: int
+    order: torch.Tensor
+    meta: torch.Tensor
+    phys: torch.Tensor
+    ks: torch.Tensor
+    vs: torch.Tensor
+    n_items: torch.Tensor
+    seq_blocks: torch.Tensor | None = None
+
+
+def decode_schedule(table: torch.Tensor, k_scale: torch.Tensor, v_scale: torch.Tensor,
+                    geom: Geometry, layer: int, B: int, p_blocks: int, *,
+                    seq_blocks: torch.Tensor | None = None, item_blocks: int | None = None,
+                    stream=None) -> DecodeSchedule:
+    """Build the sharing-aware decode schedule of `layer` from its table and scales."""
+    if k_scale.dtype != torch.float32 or v_scale.dtype != torch.float32:
+        raise InvalidCacheError("scheduled decode needs float32 scales (bf16 pools)")
+    dev = table.device
+    nh = geom.h if geom.head_mode else 1
+    ib = int(item_blocks or N.lib().kvf_decode_schedule_item_blocks())
+    nit = -(-p_blocks // ib)
+    cap = max(B * nit, 1)
+    order = torch.empty((nh, B, p_blocks), dtype=torch.int32, device=dev)
+    meta = torch.empty((nh, cap), dtype=torch.int32, device=dev)
+    phys = torch.empty((nh, cap, ib), dtype=torch.int32, device=dev)
+    ks = torch.empty((nh, cap, ib), dtype=torch.float32, device=dev)
+    vs = torch.empty((nh, cap, ib), dtype=torch.float32, device=dev)
+    n_items = torch.empty(nh, dtype=torch.int32, device=dev)
+    ws_ints = int(N.lib().kvf_decode_schedule_ws_ints(geom.head_mode, geom.h, geom.NB, B, p_blocks, ib))
+    ws = torch.empty(max(ws_ints, 1), dtype=torch.int32, device=dev)
+    N.call("kvf_decode_schedule", N.ptr(table), N.ptr(k_scale), N.ptr(v_scale), *geom.args(), layer,
+           B, p_blocks, N.ptr(seq_blocks), ib, N.ptr(order), N.ptr(meta), N.ptr(phys), N.ptr(ks),
+           N.ptr(vs), N.ptr(n_items), N.ptr(ws), ws.numel(), N.stream_ptr(stream))
+    return DecodeSchedule(layer, B, p_blocks, ib, order, meta, phys, ks, vs, n_items, seq_blocks)
+
+
+def state_decode_schedule(state: FusionState, layer: int, B: int, p_blocks: int, *,
+                          seq_blocks: torch.Tensor | None = None,
+                          item_blocks: int | None = None) -> DecodeSchedule:
+    """decode_schedule() of one layer of a fused device state."""
+    return decode_schedule(state.table, state.k_scale, state.v_scale, state.geom, layer, B, p_blocks,
+                           seq_blocks=seq_blocks, item_blocks=item_blocks)
+
+
+def _decode_sched(q: torch.Tensor, pool_k, pool_v, geom: Geometry, layer: int, table, k_scale,
+                  v_scale, sched: DecodeSchedule, Hq: int, sm_scale: float, *, out=None, lse=None,
+                  workspace=None, stream=None):
+    dt = dtype_code(pool_k.dtype)
+    acc = acc_dtype(pool_k.dtype)
+    dev = pool_k.device
+    B, p_blocks = sched.B, sched.p_blocks
+    if out is None:
+        out = torch.empty((B, Hq, geom.d), dtype=acc, device=dev)
+    if lse is None:
+        lse = torch.empty((B, Hq), dtype=acc, device=dev)
+    nit = -(-p_blocks // sched.item_blocks)
+    ws_bytes = B * Hq * nit * (geom.d + 2) * 4
+    if workspace is None or workspace.numel() < ws_bytes:
+        workspace = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+    N.call(
+        "kvf_paged_decode_sched", N.ptr(q), dtype_code(q.dtype), N.ptr(pool_k), N.ptr(pool_v), dt,
+        *geom.args(), layer, N.ptr(table), N.ptr(k_scale), N.ptr(v_scale), B, p_blocks,
+        N.ptr(sched.seq_blocks), Hq, float(sm_scale), N.ptr(out), N.ptr(lse), sched.item_blocks,
+        N.ptr(sched.meta), N.ptr(sched.phys), N.ptr(sched.ks), N.ptr(sched.vs), N.ptr(sched.n_items),
+        N.ptr(workspace), workspace.numel(), N.stream_ptr(stream),
+    )
+    return out, lse
+
+
 def paged_decode(q: torch.Tensor, state: FusionState, layer: int, B: int, p_blocks: int, *,
                  sm_scale: float | None = None, seq_blocks: torch.Tensor | None = None,
-                 out=None, lse=None, workspace=None, stream=None):
+                 schedule: DecodeSchedule | None = None, out=None, lse=None, workspace=None,
+                 stream=None):
     """Batched decode over a fused device state: q [B, Hq, d] -> out [B, Hq, d].
 
     Slot (b, j) = b * p_blocks + j of `layer`; Hq must be a multiple of the
-    KV head count (GQA group = Hq / h).
+    KV head count (GQA group = Hq / h). With a `schedule` (decode_schedule of
+    this layer's table) the sharing-aware kernel is used.
     """
     g = state.geom
     Hq = q.shape[1]
     sc = sm_scale if sm_scale is not None else 1.0 / float(np.sqrt(g.d))
+    if schedule is not None:
+        if schedule.layer != layer or schedule.B != B or schedule.p_blocks != p_blocks:
+            raise InvalidCacheError("decode schedule was built for another layer / batch shape")
+        return _decode_sched(q, state.pool_k, state.pool_v, g, layer, state.table, state.k_scale,
+                             state.v_scale, schedule, Hq, sc, out=out, lse=lse,
+                             workspace=workspace, stream=stream)
     o, l, _ = _decode(q, state.pool_k, state.pool_v, g, layer, state.table, state.k_scale,
                       state.v_scale, B, p_blocks, Hq, sc, seq_blocks=seq_blocks, out=out,
                       lse=lse, workspace=workspace, stream=stream)

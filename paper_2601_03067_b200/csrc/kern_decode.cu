@@ -419,6 +419,7 @@ static cudaError_t decode_t(const DecodeArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_paged_decode(const DecodeArgs& a, cudaStream_t s) {
+  if (a.sched != nullptr) return a.B == 0 ? cudaSuccess : launch_decode_sched(a, s);
   if (a.g.d > MAXD || a.g.t > MAXT || a.Hq % a.g.h != 0 || a.Hq / a.g.h > MAXG)
     return cudaErrorInvalidValue;
   if (a.ws_bytes < decode_workspace_size(a.dtype, a.B, a.Hq, a.g.d, a.p_blocks, a.g.t))

@@ -120,6 +120,7 @@ cudaError_t launch_refold(const void* pool, int dtype, const Geom& g, int64_t la
                           const int32_t* table, const void* scale, void* out,
                           cudaStream_t s);
 
+struct SchedView;
 int64_t decode_workspace_size(int dtype, int64_t B, int Hq, int d, int64_t p_blocks, int t);
 struct DecodeArgs {
   const void* q;
@@ -141,11 +142,39 @@ struct DecodeArgs {
   void* probs;
   void* ws;
   int64_t ws_bytes;
+  // sharing-aware schedule (kvf_decode_schedule); null = request-major path
+  const struct SchedView* sched = nullptr;
 };
 cudaError_t launch_paged_decode(const DecodeArgs& a, cudaStream_t s);
 // TMA + mma.sync decode path (kern_decode_tma.cu) and the shared split combine
 bool decode_tma_supported(const DecodeArgs& a);
 cudaError_t launch_decode_tma(const DecodeArgs& a, cudaStream_t s);
+// sharing-aware decode (kern_decode_sched.cu). A schedule lists, per head
+// unit hu (h units in per_head mode, else 1), `n_items` items of `ib` slots:
+//   meta[hu][i]          = b * nit + k  (request b, k-th item of b), items in
+//                          ascending order of their first physical block
+//   phys/ks/vs[hu][i][j] = physical block / K scale / V scale of the item's
+//                          j-th slot (slots of a request in ascending phys
+//                          order); phys = -1 marks padding past seq_blocks
+// cap = B * nit is the per-unit stride of meta (x ib for the slot arrays).
+struct SchedView {
+  const int32_t* meta;
+  const int32_t* phys;
+  const float* ks;
+  const float* vs;
+  const int32_t* n_items;
+  int64_t cap;
+  int ib;
+};
+bool decode_sched_item_blocks_ok(int ib);
+bool decode_sched_shape_ok(int t, int d);  // one block per warp tile: t in {16, 32}
+int64_t decode_schedule_ws_ints(int64_t nh, int64_t NB, int64_t B, int64_t p_blocks, int ib);
+cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, const float* v_scale,
+                                   const Geom& g, int64_t layer, int64_t B, int64_t p_blocks,
+                                   const int32_t* seq_blocks, int ib, int32_t* order,
+                                   int32_t* meta, int32_t* phys, float* ks, float* vs,
+                                   int32_t* n_items, int32_t* ws, cudaStream_t s);
+cudaError_t launch_decode_sched(const DecodeArgs& a, cudaStream_t s);
 cudaError_t launch_decode_combine(const DecodeArgs& a, int64_t nsplit, int cbs, cudaStream_t s);
 
 }  // namespace kvf

@@ -10,6 +10,7 @@
 
 using namespace kvf;
 
+
 namespace {
 thread_local std::string g_last_error;
 
@@ -294,12 +295,13 @@ int64_t kvf_decode_workspace_size(int dtype, int64_t B, int Hq, int d, int64_t p
   return decode_workspace_size(dtype, B, Hq, d, p_blocks, t);
 }
 
-int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k, const void* pool_v,
+static int paged_decode_impl(const void* q, int q_dtype, const void* pool_k, const void* pool_v,
                      int dtype, int64_t L, int64_t NB, int t, int h, int d, int head_mode,
                      int64_t layer, const int32_t* table, const void* k_scale,
                      const void* v_scale, int64_t B, int64_t p_blocks,
                      const int32_t* seq_blocks, int Hq, double sm_scale, void* out, void* lse,
-                     void* probs, void* workspace, int64_t workspace_bytes, void* stream) {
+                     void* probs, void* workspace, int64_t workspace_bytes, void* stream,
+                             const SchedView* sched) {
   DecodeArgs a;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
   if (!valid_dtype(dtype) || !valid_dtype(q_dtype)) return fail(KVF_ERR_INVALID, "bad dtype");
@@ -330,9 +332,83 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k, const void*
   a.probs = probs;
   a.ws = workspace;
   a.ws_bytes = workspace_bytes;
-  if (workspace_bytes < decode_workspace_size(dtype, B, Hq, d, p_blocks, t))
+  a.sched = sched;
+  if (sched) {
+    if (!sched->meta || !sched->phys || !sched->ks || !sched->vs || !sched->n_items)
+      return fail(KVF_ERR_INVALID, "schedule arrays must all be given");
+    if (!decode_sched_item_blocks_ok(sched->ib))
+      return fail(KVF_ERR_INVALID, "item_blocks must be 8 or 16, got %d", sched->ib);
+    if (!decode_sched_shape_ok(t, d))
+      return fail(KVF_ERR_INVALID, "scheduled decode needs t in {16, 32} and d in {64, 128}");
+    if (!decode_tma_supported(a))
+      return fail(KVF_ERR_INVALID, "scheduled decode needs bf16 pools, d in {64,128}, t | 32");
+  }
+  if (!sched && workspace_bytes < decode_workspace_size(dtype, B, Hq, d, p_blocks, t))
     return fail(KVF_ERR_INVALID, "decode workspace too small");
   return cuda_status(launch_paged_decode(a, (cudaStream_t)stream), "kvf_paged_decode");
+}
+
+int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k, const void* pool_v,
+                     int dtype, int64_t L, int64_t NB, int t, int h, int d, int head_mode,
+                     int64_t layer, const int32_t* table, const void* k_scale,
+                     const void* v_scale, int64_t B, int64_t p_blocks,
+                     const int32_t* seq_blocks, int Hq, double sm_scale, void* out, void* lse,
+                     void* probs, void* workspace, int64_t workspace_bytes, void* stream) {
+  return paged_decode_impl(q, q_dtype, pool_k, pool_v, dtype, L, NB, t, h, d, head_mode, layer,
+                           table, k_scale, v_scale, B, p_blocks, seq_blocks, Hq, sm_scale, out,
+                           lse, probs, workspace, workspace_bytes, stream, nullptr);
+}
+
+int kvf_decode_schedule_item_blocks(void) { return 16; }
+
+int64_t kvf_decode_schedule_ws_ints(int head_mode, int h, int64_t NB, int64_t B, int64_t p_blocks,
+                                    int item_blocks) {
+  if (!decode_sched_item_blocks_ok(item_blocks)) return -1;
+  return decode_schedule_ws_ints(head_mode ? h : 1, NB, B, p_blocks, item_blocks);
+}
+
+int kvf_decode_schedule(const int32_t* table, const void* k_scale, const void* v_scale, int64_t L,
+                        int64_t NB, int t, int h, int d, int head_mode, int64_t layer, int64_t B,
+                        int64_t p_blocks, const int32_t* seq_blocks, int item_blocks,
+                        int32_t* order, int32_t* meta, int32_t* phys, float* ks, float* vs,
+                        int32_t* n_items, int32_t* workspace, int64_t workspace_ints,
+                        void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (layer < 0 || layer >= L) return fail(KVF_ERR_INVALID, "layer out of range");
+  if (B < 0 || p_blocks < 1 || B * p_blocks > NB)
+    return fail(KVF_ERR_INVALID, "B*p_blocks (%lld) exceeds blocks per layer (%lld)",
+                (long long)(B * p_blocks), (long long)NB);
+  if (p_blocks > 16384) return fail(KVF_ERR_INVALID, "p_blocks > 16384 per request");
+  if (!decode_sched_item_blocks_ok(item_blocks))
+    return fail(KVF_ERR_INVALID, "item_blocks must be 8 or 16, got %d", item_blocks);
+  if (!table || !k_scale || !v_scale || !order || !meta || !phys || !ks || !vs || !n_items ||
+      !workspace)
+    return fail(KVF_ERR_INVALID, "null pointer");
+  if (workspace_ints < decode_schedule_ws_ints(head_mode ? h : 1, NB, B, p_blocks, item_blocks))
+    return fail(KVF_ERR_INVALID, "schedule workspace too small");
+  return cuda_status(launch_decode_schedule(table, (const float*)k_scale, (const float*)v_scale, g,
+                                            layer, B, p_blocks, seq_blocks, item_blocks, order,
+                                            meta, phys, ks, vs, n_items, workspace,
+                                            (cudaStream_t)stream),
+                     "kvf_decode_schedule");
+}
+
+int kvf_paged_decode_sched(const void* q, int q_dtype, const void* pool_k, const void* pool_v,
+                           int dtype, int64_t L, int64_t NB, int t, int h, int d, int head_mode,
+                           int64_t layer, const int32_t* table, const void* k_scale,
+                           const void* v_scale, int64_t B, int64_t p_blocks,
+                           const int32_t* seq_blocks, int Hq, double sm_scale, void* out,
+                           void* lse, int item_blocks, const int32_t* meta, const int32_t* phys,
+                           const float* ks, const float* vs, const int32_t* n_items,
+                           void* workspace, int64_t workspace_bytes, void* stream) {
+  const int64_t nit = item_blocks > 0 ? (p_blocks + item_blocks - 1) / item_blocks : 0;
+  SchedView v{meta, phys, ks, vs, n_items, B * nit, item_blocks};
+  if (workspace_bytes < B * Hq * nit * (int64_t)(d + 2) * 4)
+    return fail(KVF_ERR_INVALID, "decode workspace too small");
+  return paged_decode_impl(q, q_dtype, pool_k, pool_v, dtype, L, NB, t, h, d, head_mode, layer,
+                           table, k_scale, v_scale, B, p_blocks, seq_blocks, Hq, sm_scale, out,
+                           lse, nullptr, workspace, workspace_bytes, stream, &v);
 }
 
 }  // extern "C"

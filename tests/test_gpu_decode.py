@@ -77,3 +77,77 @@ def test_decode_unfused_matches_fused_when_nothing_fuses():
     got, _ = K.paged_decode(q, st, 0, B, p)
     want = _reference(q, st, 0, B, p)
     torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
+
+
+@pytest.mark.parametrize("ib", [8, 16])
+@pytest.mark.parametrize("d,G,head_mode", [(128, 4, "folded"), (64, 2, "per_head"), (128, 8, "folded")])
+def test_scheduled_decode_vs_reference(d, G, head_mode, ib):
+    """Sharing-aware schedule: same attention as the request-major reference."""
+    L, B, p, t, h = 2, 7, 45, 16, 4
+    Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=37)
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8, head_mode=head_mode), keep_samples=False)
+    st = outs[0].fused.state
+    torch.manual_seed(1)
+    q = torch.randn((B, h * G, d), device="cuda", dtype=torch.bfloat16)
+    seq = torch.tensor([p, p - 3, 1, 17, p, 5, 9], dtype=torch.int32, device="cuda")
+    nit = (p + ib - 1) // ib
+    for layer in range(L):
+        for sb in (None, seq):
+            sched = K.state_decode_schedule(st, layer, B, p, seq_blocks=sb, item_blocks=ib)
+            nh = h if head_mode == "per_head" else 1
+            nblk = (sb.long() if sb is not None else torch.full((B,), p, device="cuda")).cpu()
+            n_valid = int(sum((int(n) + ib - 1) // ib for n in nblk))
+            assert sched.n_items.cpu().tolist() == [n_valid] * nh
+            for hu in range(nh):
+                u = layer * h + hu if head_mode == "per_head" else layer
+                tab, ksc, vsc = st.table[u].cpu(), st.k_scale[u].cpu(), st.v_scale[u].cpu()
+                meta = sched.meta[hu, :n_valid].cpu().long()
+                phys = sched.phys[hu, :n_valid].cpu()
+                firsts = phys[:, 0].tolist()
+                assert firsts == sorted(firsts)  # items swept by first physical block
+                assert sorted(meta.tolist()) == sorted(
+                    b * nit + k for b in range(B) for k in range((int(nblk[b]) + ib - 1) // ib))
+                for row, it in enumerate(meta.tolist()):
+                    b, k = divmod(it, nit)
+                    pos = sched.order[hu, b, k * ib:(k + 1) * ib].cpu().long()
+                    pos = pos[(torch.arange(len(pos)) + k * ib) < int(nblk[b])]
+                    n = len(pos)
+                    assert (phys[row, n:] == -1).all()
+                    slots = b * p + pos
+                    assert torch.equal(phys[row, :n], tab[slots])
+                    assert torch.equal(sched.ks[hu, row, :n].cpu(), ksc[slots])
+                    assert torch.equal(sched.vs[hu, row, :n].cpu(), vsc[slots])
+                for b in range(B):
+                    n = int(nblk[b])
+                    o = sched.order[hu, b, :n].cpu().long()
+                    assert sorted(o.tolist()) == list(range(n))
+                    assert (sched.order[hu, b, n:] == -1).all()
+                    ph = tab[b * p + o]
+                    assert (ph[1:] >= ph[:-1]).all()
+            got, lse = K.paged_decode(q, st, layer, B, p, schedule=sched)
+            want = _reference(q, st, layer, B, p, sb)
+            torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
+            plain, lse0 = K.paged_decode(q, st, layer, B, p, seq_blocks=sb)
+            torch.testing.assert_close(got, plain, atol=1e-3, rtol=1e-3)
+            torch.testing.assert_close(lse, lse0, atol=1e-3, rtol=1e-3)
+
+
+def test_scheduled_decode_many_sharers():
+    """A batch where most slots point at a few shared blocks (high refcount)."""
+    L, B, p, t, h, d = 1, 32, 24, 16, 2, 128
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    base_k = torch.randn((4, t, h, d), device="cuda", generator=gen)
+    base_v = torch.randn((4, t, h, d), device="cuda", generator=gen)
+    pick = torch.randint(0, 4, (B, p), device="cuda", generator=gen)
+    noise = 0.02
+    Kt = (base_k[pick] + noise * torch.randn((B, p, t, h, d), device="cuda", generator=gen))[None].bfloat16()
+    Vt = (base_v[pick] + noise * torch.randn((B, p, t, h, d), device="cuda", generator=gen))[None].bfloat16()
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    st = K.fuse_batch(cache, K.FusionConfig(threshold=0.9), keep_samples=False)[0].fused.state
+    assert int(st.live_count.sum()) < B * p // 8
+    q = torch.randn((B, 4 * h, d), device="cuda", dtype=torch.bfloat16)
+    sched = K.state_decode_schedule(st, 0, B, p)
+    got, _ = K.paged_decode(q, st, 0, B, p, schedule=sched)
+    want = _reference(q, st, 0, B, p)
+    torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
