@@ -200,6 +200,59 @@ def cpu_sample_main(args):
     }))
 
 
+def cpu_decode_sample_main(calls: int = 200):
+    """Subprocess: the reference's paged_attention (attention.py:58-80) on one
+    request of the decode workload (8K context, one KV head per call, float64)."""
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT / "oracle" / "_ref"))
+    kind = "reference"
+    try:
+        from kvfuse.attention import AttentionQuery, paged_attention
+        from kvfuse.core import LayerView
+    except ImportError:
+        kind = "port"
+        sys.path.insert(0, str(ROOT / "oracle"))
+        import kvfuse_oracle as O
+
+    c = DECODE
+    rng = np.random.default_rng(5)
+    keys = rng.standard_normal((2, c["p"], c["t"], c["h"], c["d"]))
+    values = rng.standard_normal((2, c["p"], c["t"], c["h"], c["d"]))
+    qs = rng.standard_normal((calls, c["d"]))
+    if kind == "reference":
+        view = LayerView(keys, values)
+        run = lambda i: paged_attention(AttentionQuery(qs[i], head=i % c["h"]), view, row=i % 2)
+    else:
+        run = lambda i: O.paged_attention(qs[i], keys, values, i % 2, i % c["h"])
+    for i in range(5):
+        run(i)
+    t0 = time.perf_counter()
+    for i in range(calls):
+        run(i)
+    per_call = (time.perf_counter() - t0) / calls
+    print(json.dumps({"kind": kind, "per_call_s": per_call, "calls": calls}))
+
+
+def run_cpu_decode_sample():
+    env = dict(os.environ)
+    env.update(OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--cpu-decode-sample"], env=env,
+                         capture_output=True, text=True, timeout=600)
+    if res.returncode != 0:
+        raise RuntimeError(f"cpu decode sample failed: {res.stderr[-2000:]}")
+    s = json.loads(res.stdout.strip().splitlines()[-1])
+    c = DECODE
+    step_s = s["per_call_s"] * c["B"] * c["Hq"] * c["L"]  # one token for every (request, q head, layer)
+    return {"value": c["B"] / step_s, "unit": "tok/s", "cores": 1, "kind": s["kind"],
+            "sample": f"{s['calls']} paged_attention calls (one request x one query head, 8K context, "
+                      f"float64, OPENBLAS_NUM_THREADS=1) at {s['per_call_s'] * 1e3:.3f} ms each, scaled to "
+                      f"{c['B']} requests x {c['Hq']} query heads x {c['L']} layers per token step; "
+                      f"refold (core.py:285-305) excluded"}
+
+
 def run_cpu_sample(config, steps, warmup, seed=7):
     cores = os.cpu_count() or 1
     layers = max(1, min(cores, 8))
@@ -394,6 +447,11 @@ def ours_main(args):
     torch.cuda.empty_cache()
     if rank == 0 and not args.skip_decode:
         out["decode"] = bench_decode(dev, torch)
+        if not args.skip_cpu:
+            try:
+                out["decode"]["cpu_baseline"] = run_cpu_decode_sample()
+            except Exception as exc:  # reported, never fatal
+                out["decode"]["cpu_baseline"] = {"value": None, "error": str(exc)[-300:]}
     if rank == 0 and not args.skip_cpu:
         try:
             s = run_cpu_sample(args.config, steps=2, warmup=1)
@@ -563,12 +621,15 @@ def main():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-decode", action="store_true")
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--cpu-decode-sample", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--sample-layers", type=int, default=8, help=argparse.SUPPRESS)
     ap.add_argument("--sample-B", type=int, default=16, help=argparse.SUPPRESS)
     ap.add_argument("--seed", type=int, default=7, help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.cpu_sample:
         return cpu_sample_main(args)
+    if args.cpu_decode_sample:
+        return cpu_decode_sample_main()
     if args.impl == "reference":
         return reference_main(args)
     return ours_main(args)
