@@ -40,6 +40,10 @@ CONFIGS = {
     # configs[2]: CFF, 8 chunks x 2K tokens per request, Llama-3-8B shape
     "cfg3": dict(workload="cff_llama3_8b_8x2k", L=32, B=1, p=1024, t=16, h=8, d=128,
                  dtype="bf16", variant="cff", thr=0.8, chunk_tokens=2048),
+    # configs[4]: Llama-3-70B KV, batch 256 x 16K, layers sharded over the ranks and
+    # streamed through each GPU (1.37 TB of K+V does not fit in HBM)
+    "cfg5": dict(workload="bff_llama3_70b_bs256_ctx16k_layer_sharded", L=80, B=256, p=1024, t=16,
+                 h=8, d=128, dtype="bf16", variant="bff", thr=0.8, chunk_tokens=None),
 }
 METRIC = "KV GB/s fused (BFF/CFF) + compression ratio; fused-cache decode attention tok/s"
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
@@ -414,7 +418,8 @@ def ours_main(args):
                 "workload": c["workload"], "L": L, "B": B, "p": p, "t": t, "h": h, "d": d,
                 "threshold": c["thr"], "variant": c["variant"], "head_mode": args.head_mode,
                 "parallelism": f"replicas x{world} (weak; layer units independent, NCCL gathers counters)",
-                "l2": "inputs 34 GB >> 126 MB L2; pristine-pool restore copy between steps (untimed)",
+                "l2": f"inputs {kv_bytes(c, elem) / 1e9:.1f} GB >> 126 MB L2; pristine-pool restore copy "
+                      "between steps (untimed)",
                 "timing": "sum of per-step CUDA-event intervals on the launch stream, max over ranks",
             },
             "compression_ratio": cr,
@@ -608,6 +613,120 @@ def bench_e2e(args, c, K0, V0, dtype, dev, world, torch, dist, PagedKvCache, Cac
                     "in 4-layer chunks under fusion) -> table/refcount/scales .cpu()"}
 
 
+def ours_cfg5(args):
+    """BASELINE configs[4]: BFF of a Llama-3-70B-shaped KV cache (80 layers x 8 KV
+    heads x d = 128, batch 256 x 16K, bf16), layers sharded contiguously over
+    the ranks (strong scaling: 80 layers in total for any N). Each layer's K/V
+    (17.2 GB) is produced on the GPU (stand-in for its arrival from prefill,
+    untimed), fused (timed, CUDA events), its counters kept, and freed; the
+    per-step NCCL all_gather of per-layer block counts is the only collective
+    (SURVEY §8e). --layers-per-rank K times K of the rank's layers per step and
+    scales the time to its full share (stated in `config`)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2601_03067_b200.dist import shard_units
+    from paper_2601_03067_b200.engine import FusionEngine, Geometry
+    from paper_2601_03067_b200.schedule import bff_plan
+    from paper_2601_03067_b200.workload import synthetic_kv
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS["cfg5"]
+    L, B, p, t, h, d = c["L"], c["B"], c["p"], c["t"], c["h"], c["d"]
+    mine = list(shard_units(L, world, rank))
+    run = mine[: args.layers_per_rank] if args.layers_per_rank else mine
+    geom = Geometry(1, B * p, t, h, d, 0)
+    engine = FusionEngine(geom, bff_plan(B, p, None), torch.bfloat16, dev)
+    n_max = -(-L // world)
+    live = torch.zeros(n_max, dtype=torch.int32, device=dev)
+    gathered = torch.empty((world, n_max), dtype=torch.int32, device=dev)
+
+    def step(timed):
+        ms, flops, launches = 0.0, 0.0, 0
+        sim_ms = 0.0
+        for i, layer in enumerate(run):
+            K, V = synthetic_kv(1, B, p, t, h, d, dtype=torch.bfloat16, seed=3000 + layer, device=dev)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = engine.run(K.view(-1), V.view(-1), c["thr"], time_sim=timed)
+            live[i] = st.live_count[0]
+            e1.record()
+            torch.cuda.synchronize()
+            ms += e0.elapsed_time(e1)
+            launches += st.launches
+            if timed:
+                sim_ms += sum(a.elapsed_time(b) for a, b, _ in st.sim_events)
+                flops += sum(float((2.0 * s[..., 0].double() * s[..., 1].double()).sum()) for s in st.level_stats) * geom.r
+            del K, V, st
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, live)
+        else:
+            gathered[0].copy_(live)
+        e1.record()
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+        return ms, sim_ms, flops, launches
+
+    for _ in range(args.warmup):
+        step(False)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    res = [step(True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    # time of the rank's full layer share (scaled when only a sample of it ran)
+    scale = len(mine) / len(run)
+    ms_step = sum(r[0] for r in res) / args.steps * scale
+    tmax = torch.tensor([ms_step], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    ms_step = float(tmax.item())
+    sim_ms = sum(r[1] for r in res)
+    flops = sum(r[2] for r in res)
+    total_bytes = kv_bytes(c, 2)  # all 80 layers, K + V
+    counts = gathered.cpu()
+    per_rank_live = [int(counts[r, : len(shard_units(L, world, r)[: len(run)])].sum()) for r in range(world)]
+    cr = (world * len(run) * B * p) / max(1, sum(per_rank_live))
+    if rank == 0:
+        pk = peaks()
+        tc_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+        achieved = flops / (sim_ms / 1e3) / 1e12 if sim_ms else 0.0
+        out = {
+            "metric": METRIC, "value": total_bytes / (ms_step / 1e3) / 1e9, "unit": "GB/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic clustered KV (SURVEY §8d generator, seed 3000+layer), generated per layer on the GPU",
+            "config": {"workload": c["workload"], "L": L, "B": B, "p": p, "t": t, "h": h, "d": d,
+                       "threshold": c["thr"], "variant": "bff", "head_mode": "folded",
+                       "parallelism": f"layer-sharded x{world} ({len(mine)} layers on rank 0)",
+                       "layers_timed_per_rank": len(run),
+                       "timing": "sum over the rank's layers of the CUDA-event fusion time (layer generation "
+                                 "untimed) + the NCCL stats all_gather, x layers_share/layers_timed, max over ranks",
+                       "l2": "per-layer K+V 17.2 GB >> 126 MB L2"},
+            "compression_ratio": cr,
+            "roofline": {"kernel": "sim_tc_kernel", "bound": "tensor", "achieved": achieved, "peak": tc_peak,
+                         "unit": "TFLOP/s", "frac": achieved / tc_peak if tc_peak else None, "traffic": None,
+                         "sim_share_of_step": sim_ms / sum(r[0] for r in res)},
+            "gpu_launches": sum(r[3] for r in res),
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
@@ -625,6 +744,8 @@ def main():
     ap.add_argument("--sample-layers", type=int, default=8, help=argparse.SUPPRESS)
     ap.add_argument("--sample-B", type=int, default=16, help=argparse.SUPPRESS)
     ap.add_argument("--seed", type=int, default=7, help=argparse.SUPPRESS)
+    ap.add_argument("--layers-per-rank", type=int, default=None,
+                    help="cfg5: fuse this many of the rank's layers per step and scale to its share")
     args = ap.parse_args()
     if args.cpu_sample:
         return cpu_sample_main(args)
@@ -632,6 +753,8 @@ def main():
         return cpu_decode_sample_main()
     if args.impl == "reference":
         return reference_main(args)
+    if args.config == "cfg5":
+        return ours_cfg5(args)
     return ours_main(args)
 
 
