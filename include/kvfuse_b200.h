@@ -207,6 +207,15 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
                      void* out, void* lse, void* probs, void* workspace,
                      int64_t workspace_bytes, void* stream);
 
+/* Compaction of a fused layer (the reference's FusedCache storage: live
+ * blocks only, ascending physical id, core.py:246-270 / fusion.py:318-327):
+ * kvf_alive_rank gives the ascending live ids and the exclusive alive rank of
+ * every block, kvf_stage_rows copies the live rows densely (bf16, folded), and
+ * kvf_remap_ids maps slot tables and decode-schedule ids to dense rows:
+ * out[i] = map[ids[i]] for 0 <= ids[i] < map_len, else -1. */
+int kvf_remap_ids(const int32_t* ids, int64_t n, const int32_t* map,
+                  int64_t map_len, int32_t* out, void* stream);
+
 /* Sharing-aware decode schedule (PAPER.md:56, 130-131:
  * a fused block shared by several requests should be fetched once). For
  * serving batches it replaces the request-major loop of attention.py:58-80;

@@ -429,6 +429,24 @@ __global__ void sched_scatter_kernel(const int32_t* __restrict__ item_key,
 
 bool decode_sched_item_blocks_ok(int ib) { return ib == 8 || ib == 16; }
 
+__global__ void remap_ids_kernel(const int32_t* __restrict__ ids, int64_t n,
+                                 const int32_t* __restrict__ map, int64_t map_len,
+                                 int32_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = ids[i];
+    out[i] = (x >= 0 && x < map_len) ? map[x] : -1;
+  }
+}
+
+cudaError_t launch_remap_ids(const int32_t* ids, int64_t n, const int32_t* map, int64_t map_len,
+                             int32_t* out, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, 4096);
+  remap_ids_kernel<<<(unsigned)blocks, 256, 0, s>>>(ids, n, map, map_len, out);
+  return cudaGetLastError();
+}
+
 int64_t decode_schedule_ws_ints(int64_t nh, int64_t NB, int64_t B, int64_t p_blocks, int ib) {
   return nh * NB + nh * B * ((p_blocks + ib - 1) / ib);
 }

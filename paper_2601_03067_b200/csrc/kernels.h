@@ -175,6 +175,10 @@ cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, c
                                    int32_t* meta, int32_t* phys, float* ks, float* vs,
                                    int32_t* n_items, int32_t* ws, cudaStream_t s);
 cudaError_t launch_decode_sched(const DecodeArgs& a, cudaStream_t s);
+// out[i] = map[ids[i]] for 0 <= ids[i] < map_len, else -1 (compaction: slot
+// tables / schedule ids -> dense rows of a compacted pool)
+cudaError_t launch_remap_ids(const int32_t* ids, int64_t n, const int32_t* map, int64_t map_len,
+                             int32_t* out, cudaStream_t s);
 cudaError_t launch_decode_combine(const DecodeArgs& a, int64_t nsplit, int cbs, cudaStream_t s);
 
 }  // namespace kvf

@@ -310,7 +310,10 @@ static int paged_decode_impl(const void* q, int q_dtype, const void* pool_k, con
     return fail(KVF_ERR_INVALID, "query heads %d must be a positive multiple of kv heads %d", Hq, h);
   if (Hq / h > 8 || d > 128 || t > 32)
     return fail(KVF_ERR_INVALID, "decode kernel limits: Hq/h <= 8, d <= 128, t <= 32");
-  if (B < 0 || p_blocks < 1 || B * p_blocks > NB)
+  // the request-major path reads table[unit][b * p_blocks + j]; the scheduled
+  // path reads only the schedule's physical ids (< NB), so a compacted pool
+  // (NB = live blocks < slots) is allowed there
+  if (B < 0 || p_blocks < 1 || (!sched && B * p_blocks > NB))
     return fail(KVF_ERR_INVALID, "B*p_blocks (%lld) exceeds blocks per layer (%lld)",
                 (long long)(B * p_blocks), (long long)NB);
   a.q = q;
@@ -357,6 +360,14 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k, const void*
   return paged_decode_impl(q, q_dtype, pool_k, pool_v, dtype, L, NB, t, h, d, head_mode, layer,
                            table, k_scale, v_scale, B, p_blocks, seq_blocks, Hq, sm_scale, out,
                            lse, probs, workspace, workspace_bytes, stream, nullptr);
+}
+
+int kvf_remap_ids(const int32_t* ids, int64_t n, const int32_t* map, int64_t map_len, int32_t* out,
+                  void* stream) {
+  if (n < 0 || map_len < 0) return fail(KVF_ERR_INVALID, "negative length");
+  if (n > 0 && (!ids || !map || !out)) return fail(KVF_ERR_INVALID, "null pointer");
+  return cuda_status(launch_remap_ids(ids, n, map, map_len, out, (cudaStream_t)stream),
+                     "kvf_remap_ids");
 }
 
 int kvf_decode_schedule_item_blocks(void) { return 16; }

@@ -60,3 +60,32 @@ def kv_bytes(L: int, B: int, p: int, t: int, h: int, d: int, dtype: torch.dtype)
 
 def noise_sigma(c: float, r: int) -> float:
     return math.sqrt((1.0 / (c * c) - 1.0) / r)
+
+
+def synthetic_layer_into(K: torch.Tensor, V: torch.Tensor, *, seed: int = 0, c_lo: float = 0.80,
+                         c_hi: float = 0.99, cluster_div: int = 4, chunk_rows: int = 8192) -> None:
+    """Fill one BFF layer K, V [n, ...] in place with the synthetic_kv recipe,
+    generating `chunk_rows` blocks at a time (bounded transient memory for
+    caches that only just fit; the random stream differs from synthetic_kv)."""
+    n = K.shape[0]
+    r = K[0].numel()
+    dev = K.device
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(seed & 0x7FFF_FFFF_FFFF)
+    nc = max(1, n // cluster_div)
+    assign = torch.randint(0, nc, (n,), generator=gen, device=dev)
+    for out in (K, V):
+        bases = torch.randn((nc, r), generator=gen, device=dev)
+        bases = (bases / bases.norm(dim=1, keepdim=True)).to(torch.bfloat16)
+        flat = out.view(n, r)
+        for i0 in range(0, n, chunk_rows):
+            i1 = min(n, i0 + chunk_rows)
+            m = i1 - i0
+            c = c_lo + (c_hi - c_lo) * torch.rand((m, 1), generator=gen, device=dev)
+            sigma = torch.sqrt((1.0 / (c * c) - 1.0) / r)
+            x = bases[assign[i0:i1]].float() + sigma * torch.randn((m, r), generator=gen, device=dev)
+            x = x / x.norm(dim=1, keepdim=True)
+            x = x * torch.exp(0.25 * torch.randn((m, 1), generator=gen, device=dev))
+            flat[i0:i1].copy_(x.to(out.dtype))
+            del x
+        del bases
