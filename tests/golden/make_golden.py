@@ -28,7 +28,8 @@ def main() -> None:
     import kvfuse
     from kvfuse.attention import AttentionQuery, paged_attention
     from kvfuse.core import CacheDims, LayerView, PagedKvCache, UnfoldedLayer, refold, unfold_bff
-    from kvfuse.fusion import FusionConfig, fast_fusion, fuse_batch, fuse_chunks
+    from kvfuse.fusion import (AdaptPolicy, FusionConfig, FusionReport, fast_fusion, fuse_batch,
+                               fuse_chunks, reports_to_csv, tune_threshold)
     from kvfuse.workload import generate_fixture
 
     arrays: dict[str, np.ndarray] = {}
@@ -174,8 +175,18 @@ def main() -> None:
         arrays[f"att/{i}/probs_base"] = s_b.probs
         att.append(dict(i=i, head=head, row=row))
 
+    # 7. threshold controller (acceptance 11) and report serialization (test_fusion.py:331-360)
+    policy = AdaptPolicy(mode="target-compression", target=2.0, step=0.001,
+                         min_threshold=0.85, max_threshold=0.97)
+    thr, history = tune_threshold(generate_fixture("clusters4"), FusionConfig(threshold=0.90), policy,
+                                  rel_tol=0.1, max_iters=30)
+    reports = [o.report for o in fuse_batch(generate_fixture("clusters4"), FusionConfig(threshold=0.91))]
+    agg = FusionReport.aggregate(reports)
+    host = dict(tune=dict(final=thr, history=history), csv=reports_to_csv(reports),
+                json=[r.to_json() for r in reports], aggregate=agg.to_dict())
+
     meta = dict(reference_version=kvfuse.__version__, numpy=np.__version__, cases=cases,
-                attention=att)
+                attention=att, host=host)
     np.savez_compressed(OUT / "golden.npz", **arrays)
     (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True) + "\n")
     print(f"wrote {len(cases)} cases, {len(arrays)} arrays")

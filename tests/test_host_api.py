@@ -1,0 +1,113 @@
+"""Host-side API of the drop-in (fusion.py:49-110, 126-202, 418-465): threshold
+controller, configuration validation, report serialization. CPU tests mirror
+the reference's test_fusion.py:240-360; the GPU tests replay acceptance 11
+(tune_threshold) and the JSON / CSV / aggregate reports against the reference's
+own outputs recorded in tests/golden (make_golden.py section 7)."""
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+import paper_2601_03067_b200 as K
+from paper_2601_03067_b200 import AdaptPolicy, ConfigError, FusionConfig, FusionReport, adapt_threshold
+from paper_2601_03067_b200.errors import InsufficientDataError
+
+
+def _report(samples, cr=1.0):
+    blocks = 10
+    return FusionReport(0, blocks, int(round(blocks / cr)), [], 1, 1,
+                        np.asarray(samples, dtype=np.float64))
+
+
+def test_adapt_policy_validation():
+    with pytest.raises(ConfigError):
+        AdaptPolicy(mode="nope", target=2.0, step=0.01, min_threshold=0.1, max_threshold=0.9)
+    with pytest.raises(ConfigError):
+        AdaptPolicy(mode="percentile", target=0.2, step=0.0, min_threshold=0.1, max_threshold=0.9)
+    with pytest.raises(ConfigError):
+        AdaptPolicy(mode="percentile", target=0.2, step=0.1, min_threshold=0.9, max_threshold=0.1)
+
+
+@pytest.mark.parametrize("thr", [-1.0, 1.0, 1.5, -2.0])
+def test_threshold_range(thr):
+    with pytest.raises(ConfigError):
+        FusionConfig(threshold=thr)
+
+
+def test_config_validation():
+    with pytest.raises(ConfigError):
+        FusionConfig(threshold=0.5, variant="xff")
+    with pytest.raises(ConfigError):
+        FusionConfig(threshold=0.5, group_size=0)
+
+
+def test_percentile_mode():
+    pol = AdaptPolicy(mode="percentile", target=0.2, step=0.01, min_threshold=0.0, max_threshold=0.99)
+    rep = _report(np.arange(1, 11) / 10.0)
+    assert adapt_threshold(pol, rep, 0.5) == pytest.approx(0.82)  # 0.8-quantile, linear
+    pol = AdaptPolicy(mode="percentile", target=0.2, step=0.01, min_threshold=0.0, max_threshold=0.5)
+    assert adapt_threshold(pol, rep, 0.5) == 0.5
+    with pytest.raises(InsufficientDataError):
+        adapt_threshold(pol, _report([]), 0.5)
+
+
+def test_target_compression_steps():
+    pol = AdaptPolicy(mode="target-compression", target=2.0, step=0.01, min_threshold=0.1,
+                      max_threshold=0.9)
+    hi, lo = _report([0.5], cr=5.0), _report([0.5], cr=1.25)
+    assert adapt_threshold(pol, hi, 0.5) == pytest.approx(0.51)
+    assert adapt_threshold(pol, lo, 0.5) == pytest.approx(0.49)
+    assert adapt_threshold(pol, hi, 0.9) == 0.9
+    assert adapt_threshold(pol, lo, 0.1) == 0.1
+
+
+def _clusters4():
+    arrays, _ = golden()
+    k = arrays["fixture/clusters4/keys"]
+    v = arrays["fixture/clusters4/values"]
+    L, B, p, t, h, d = k.shape
+    return K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), k, v)
+
+
+@pytest.mark.gpu
+def test_tune_threshold_matches_reference():
+    """Acceptance 11: same threshold trajectory and CRs as the reference."""
+    want = golden()[1]["host"]["tune"]
+    pol = AdaptPolicy(mode="target-compression", target=2.0, step=0.001, min_threshold=0.85,
+                      max_threshold=0.97)
+    thr, hist = K.tune_threshold(_clusters4(), FusionConfig(threshold=0.90), pol, rel_tol=0.1,
+                                 max_iters=30)
+    assert thr == want["final"]
+    assert [list(h) for h in hist] == want["history"]
+    with pytest.raises(ConfigError):
+        K.tune_threshold(_clusters4(), FusionConfig(threshold=0.9),
+                         AdaptPolicy(mode="percentile", target=0.2, step=0.01, min_threshold=0.1,
+                                     max_threshold=0.9))
+
+
+def _close(a, b):
+    if isinstance(a, dict):
+        assert a.keys() == b.keys()
+        for k in a:
+            _close(a[k], b[k])
+    elif isinstance(a, list):
+        assert len(a) == len(b)
+        for x, y in zip(a, b):
+            _close(x, y)
+    elif isinstance(a, float) and isinstance(b, float):
+        assert a == pytest.approx(b, abs=1e-12, rel=1e-12)
+    else:
+        assert a == b
+
+
+@pytest.mark.gpu
+def test_reports_json_csv_aggregate_match_reference():
+    host = golden()[1]["host"]
+    reports = [o.report for o in K.fuse_batch(_clusters4(), FusionConfig(threshold=0.91))]
+    assert K.reports_to_csv(reports) == host["csv"]
+    for r, want in zip(reports, host["json"]):
+        _close(json.loads(r.to_json()), json.loads(want))
+    _close(FusionReport.aggregate(reports).to_dict(), host["aggregate"])
