@@ -62,7 +62,7 @@ __device__ __forceinline__ void load_q_frags(uint32_t (&qa)[D / 16][2], const vo
 }
 }  // namespace
 
-template <int D, int T, int DW, int DNS, int IB>
+template <int D, int T, int BPT, int DW, int DNS, int IB>
 __global__ void __launch_bounds__(DW * 32)
 decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                     const void* __restrict__ q, int q_dtype, Geom g, int64_t layer, int64_t B,
@@ -71,14 +71,15 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
                     const float* __restrict__ svs, const int32_t* __restrict__ n_items_p,
                     int64_t cap, float* __restrict__ part) {
   static_assert(2 * IB <= 32, "slot metadata of two items must fit in one warp");
-  static_assert(T == 16 || T == 32, "one block (16 or 32 tokens) per warp tile");
-  static_assert(IB >= DNS - 1, "the copy lookahead may not pass the next item");
+  static_assert(T == 16 || T == 32, "blocks of 16 or 32 tokens");
+  static_assert(IB % BPT == 0 && IB / BPT >= DNS - 1, "the copy lookahead may not pass the next item");
   constexpr int HALVES = D / 64;
   constexpr int KS = D / 16;   // k-steps of S^T = K Q^T (head dim)
-  constexpr int MT = T / 16;   // token m-tiles of S^T = k-steps of O^T = V^T P^T
+  constexpr int MT = BPT * T / 16;  // token m-tiles of S^T = k-steps of O^T = V^T P^T
+  constexpr int TPI = IB / BPT;     // warp tiles per item
   constexpr int DT = D / 16;   // head-dim m-tiles of O^T
   constexpr int BOX = T * 128;                 // one (block, d half) box
-  constexpr int TENS = HALVES * BOX;           // one block's K (or V) head slice
+  constexpr int TENS = BPT * HALVES * BOX;     // the tile's K (or V) head slices
   constexpr int STAGE = 2 * TENS;
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~(uintptr_t)1023);
@@ -133,21 +134,27 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
   int64_t is_n = 0, cur_n = 0;
   auto issue_next = [&]() {  // all lanes (shuffle); lane 0 issues the copies
     if (is_n >= my_items) return;
-    const int32_t ph = __shfl_sync(0xffffffffu, phys_l, is_par * IB + is_j);
+    int32_t ph[BPT];
+#pragma unroll
+    for (int bb = 0; bb < BPT; ++bb)
+      ph[bb] = __shfl_sync(0xffffffffu, phys_l, is_par * IB + is_j * BPT + bb);
     if (lane == 0) {
       const int kvh = is_n == cur_n ? kvh_cur : kvh_nxt;  // issue runs at most one item ahead
       uint8_t* st = wst + (size_t)is_stage * STAGE;
-      const int row = rowbase + (ph < 0 ? 0 : ph);  // padding loads block 0 (p = 0)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[is_stage], (uint32_t)STAGE);
 #pragma unroll
-      for (int hf = 0; hf < HALVES; ++hf) {
-        tma4(st + hf * BOX, &kmap, &bars[is_stage], hf * 64, kvh, 0, row);
-        tma4(st + TENS + hf * BOX, &vmap, &bars[is_stage], hf * 64, kvh, 0, row);
+      for (int bb = 0; bb < BPT; ++bb) {
+        const int row = rowbase + (ph[bb] < 0 ? 0 : ph[bb]);  // padding loads block 0 (p = 0)
+#pragma unroll
+        for (int hf = 0; hf < HALVES; ++hf) {
+          tma4(st + (bb * HALVES + hf) * BOX, &kmap, &bars[is_stage], hf * 64, kvh, 0, row);
+          tma4(st + TENS + (bb * HALVES + hf) * BOX, &vmap, &bars[is_stage], hf * 64, kvh, 0, row);
+        }
       }
     }
     if (++is_stage == DNS) is_stage = 0;
-    if (++is_j == IB) {
+    if (++is_j == TPI) {
       is_j = 0;
       is_par ^= 1;
       ++is_n;
@@ -155,10 +162,10 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
   };
   for (int i = 0; i < DNS - 1; ++i) issue_next();
   const int lr = lane & 7, lm = lane >> 3;
-  // swizzled smem address of (token, element) inside a block's head slice
+  // swizzled smem address of (token, element) inside the tile's head slices
   auto addr = [&](uint32_t base, int tok, int e) {
-    const int hf = e >> 6, ch = (e & 63) >> 3;
-    return base + (uint32_t)(hf * BOX + tok * 128 + ((ch ^ (tok & 7)) << 4));
+    const int hf = e >> 6, ch = (e & 63) >> 3, bb = tok / T, tr = tok % T;
+    return base + (uint32_t)((bb * HALVES + hf) * BOX + tr * 128 + ((ch ^ (tr & 7)) << 4));
   };
   int cs_stage = 0;
   uint32_t cs_phase = 0;
@@ -185,14 +192,19 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
       for (int c = 0; c < 4; ++c) o[mt][c] = 0.f;
 
 #pragma unroll 1
-    for (int j = 0; j < IB; ++j) {
+    for (int j = 0; j < TPI; ++j) {
       issue_next();
       if (j == 1 && has_next)  // next item's query rows, consumed after this item
         load_q_frags<D>(qn, q, q_dtype, meta_nxt / nit, kvh_nxt, G, Hq, grp, tig);
-      const int src = par * IB + j;
-      const int32_t phv = __shfl_sync(0xffffffffu, phys_l, src);
-      const float ksv = __shfl_sync(0xffffffffu, ks_l, src);
-      const float vsv = __shfl_sync(0xffffffffu, vs_l, src);
+      bool valid[BPT];  // padding slot: contributes nothing
+      float ksv[BPT], vsv[BPT];
+#pragma unroll
+      for (int bb = 0; bb < BPT; ++bb) {
+        const int src = par * IB + j * BPT + bb;
+        valid[bb] = __shfl_sync(0xffffffffu, phys_l, src) >= 0;
+        ksv[bb] = __shfl_sync(0xffffffffu, ks_l, src);
+        vsv[bb] = __shfl_sync(0xffffffffu, vs_l, src);
+      }
       mbar_wait(&bars[cs_stage], cs_phase);
       const uint32_t kb = su32(wst + (size_t)cs_stage * STAGE);
       const uint32_t vb = kb + TENS;
@@ -219,13 +231,13 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
         }
       }
       // ---- online softmax per head (column); tokens spread over lanes (grp) ----
-      const bool valid = phv >= 0;  // padding slot: contributes nothing
       float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          const float lg = valid ? (sa[mt][c] + sb[mt][c]) * ksv : -INFINITY;
+          const int bb = mt * 16 / T;
+          const float lg = valid[bb] ? (sa[mt][c] + sb[mt][c]) * ksv[bb] : -INFINITY;
           sa[mt][c] = lg;
           mx[c & 1] = fmaxf(mx[c & 1], lg);
         }
@@ -250,8 +262,9 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
           pr[c] = m == -INFINITY ? 0.f : __expf(sa[mt][c] - m);
           l_run[c & 1] += pr[c];
         }
-        pb[mt][0] = pack_bf16(pr[0] * vsv, pr[1] * vsv);
-        pb[mt][1] = pack_bf16(pr[2] * vsv, pr[3] * vsv);
+        const float vv = vsv[mt * 16 / T];
+        pb[mt][0] = pack_bf16(pr[0] * vv, pr[1] * vv);
+        pb[mt][1] = pack_bf16(pr[2] * vv, pr[3] * vv);
       }
 #pragma unroll
       for (int mt = 0; mt < DT; ++mt) {
@@ -483,13 +496,13 @@ cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, c
 }
 
 namespace {
-template <int D, int T, int DW, int DNS, int IB>
+template <int D, int T, int BPT, int DW, int DNS, int IB>
 cudaError_t decode_sched_t(const DecodeArgs& a, cudaStream_t s) {
   CUtensorMap km, vm;
   if (!make_map(&km, a.pool_k, a.g) || !make_map(&vm, a.pool_v, a.g)) return cudaErrorInvalidValue;
-  constexpr int STAGE = 2 * (D / 64) * T * 128;
+  constexpr int STAGE = 2 * BPT * (D / 64) * T * 128;
   constexpr int smem = 1024 + DW * DNS * STAGE + DW * DNS * 8;
-  auto kern = decode_sched_kernel<D, T, DW, DNS, IB>;
+  auto kern = decode_sched_kernel<D, T, BPT, DW, DNS, IB>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -521,13 +534,13 @@ cudaError_t decode_sched_t(const DecodeArgs& a, cudaStream_t s) {
 
 template <int D, int T>
 cudaError_t decode_sched_ib(const DecodeArgs& a, cudaStream_t s) {
-  // 16-token blocks: 8 KB stages, 12 warps x 2 stages (192 KB) -- measured on
-  // B200 at batch 64 x 4K: 8 x 3 143.6 us, 12 x 2 121.8 us, 14 x 2 122.8 us per
-  // layer (the warp loop is issue-latency bound, more warps beat deeper rings);
-  // 32-token blocks: 16 KB stages, 6 warps x 2 stages
+  // one block per warp tile; 16-token blocks: 8 KB stages, 12 warps x 2 stages.
+  // Measured on B200 at batch 64 x 4K (us per layer): 8 warps x 3 stages 143.6,
+  // 12 x 2 121.8, 14 x 2 122.8; two blocks per tile: 6 x 2 141.0, 4 x 3 164.4
+  // (the warp loop is latency bound: warps per SM beat deeper rings and tiles).
   constexpr int DW = T == 16 ? 12 : 6;
-  if (a.sched->ib == 16) return decode_sched_t<D, T, DW, 2, 16>(a, s);
-  if (a.sched->ib == 8) return decode_sched_t<D, T, DW, 2, 8>(a, s);
+  if (a.sched->ib == 16) return decode_sched_t<D, T, 1, DW, 2, 16>(a, s);
+  if (a.sched->ib == 8) return decode_sched_t<D, T, 1, DW, 2, 8>(a, s);
   return cudaErrorInvalidValue;
 }
 }  // namespace
