@@ -84,9 +84,10 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
  * samples (optional, out): double, samples[(u-u0)*sample_stride +
  *   sample_off[m] + il*right_n + jl] = sim or NaN for masked pairs (compacted
  *   launches leave dead pairs untouched: pre-fill with NaN).
- * Compaction (tcgen05 path only; all three or none): live/rank from
- * kvf_alive_rank and staged from kvf_stage_rows -- tiles then index the
- * merge's alive blocks only and operands stream from the staged rows.
+ * Compaction (tcgen05 path only): live/rank from kvf_alive_rank -- tiles
+ * then index the merge's alive blocks only. With staged (kvf_stage_rows) the
+ * operands stream from the staged dense rows; with staged == NULL (folded
+ * units) they are gathered straight from the pool with TMA gather4.
  * Re-score (tcgen05 path): pairs with |sim - thr| <= rescore_band are queued
  * (int32[4 * (rescore_cap + 1)], entries then the count) and decided from a
  * float64 recomputation in the same call; NULL / 0 disables it. */

@@ -84,6 +84,18 @@ __device__ __forceinline__ void tma_load_4d_2sm(void* dst, const CUtensorMap* ma
       "r"(c2), "r"(c3)
       : "memory");
 }
+// 2-SM TMA gather4: rows r[0..3] x 64 columns of a 2-D map into 4 consecutive
+// 128 B smem rows (the 128B swizzle follows the smem address, so 32 gathers at
+// 512 B steps lay out exactly like one 128-row box)
+__device__ __forceinline__ void tma_gather4_2sm(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int col, const int (&r)[4]) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(col), "r"(r[0]),
+      "r"(r[1]), "r"(r[2]), "r"(r[3])
+      : "memory");
+}
 // K-major, 128B-swizzled UMMA shared-memory descriptor: SBO = 1024 B (8 rows
 // x 128 B), LBO unused (1), version 1 (sm_100), layout SWIZZLE_128B (2).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -208,7 +220,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               const int64_t* __restrict__ sample_off, int64_t sample_stride,
               const int32_t* __restrict__ live, const int32_t* __restrict__ rank,
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
-              float resc_band, int32_t* __restrict__ work_counter) {
+              float resc_band, int32_t* __restrict__ work_counter, int gathered) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* meta = smem + STAGES * STAGE_BYTES;
@@ -229,7 +241,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
   const bool leader = crank == 0;
-  const bool staged = live != nullptr;
+  const bool staged = live != nullptr;  // tiles index alive positions (staged or gathered rows)
   const int nwork = (int)(nt * nU);
   const int P = (int)(gridDim.x >> 1);
   const int layer_div = g.head_mode ? g.h : 1;
@@ -263,14 +275,17 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
+    // producer warp: lane 0 runs the tile scheduler; operand rows are loaded by
+    // lane 0 (tiled boxes over the pool or the staged rows) or, in gathered
+    // mode, by all 32 lanes with TMA gather4 (4 alive rows per lane per operand)
+    if (lane == 0)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-      uint32_t kk = 0;  // global k-step counter (ring position)
-      for (uint32_t it = 0;; ++it) {
-        const int sl = it % SCHED_DEPTH;
-        const uint32_t sph = (it / SCHED_DEPTH) & 1;
-        int w;
-        TileInfo t;
+    uint32_t kk = 0;  // global k-step counter (ring position)
+    for (uint32_t it = 0;; ++it) {
+      const int sl = it % SCHED_DEPTH;
+      const uint32_t sph = (it / SCHED_DEPTH) & 1;
+      int w = 0;
+      if (lane == 0) {
         if (leader) {  // fetch the next tile with alive blocks; publish it to both CTAs
           mbar_wait_cluster(&sched_empty[sl], sph ^ 1);
           for (;;) {
@@ -280,10 +295,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               w = -1;
               break;
             }
-            t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
-            if (t.active) break;
-            const int tile = w - (int)t.ul * nt;  // tile fully beyond the alive blocks
-            double* pp = partials + ((int64_t)t.ul * 2 * nt + 2 * tile) * 5;
+            const TileInfo t0 = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+            if (t0.active) break;
+            const int tile = w - (int)t0.ul * nt;  // tile fully beyond the alive blocks
+            double* pp = partials + ((int64_t)t0.ul * 2 * nt + 2 * tile) * 5;
             for (int q = 0; q < 2; ++q) {
               pp[5 * q + 0] = pp[5 * q + 1] = pp[5 * q + 2] = 0.0;
               pp[5 * q + 3] = INFINITY;
@@ -298,32 +313,63 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
           mbar_wait_cluster(&sched_full[sl], sph);
           w = sched_w[sl];
           mbar_arrive_cluster(&sched_empty[sl], 0);
-          if (w >= 0) t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
         }
-        if (w < 0) break;
-        const int layer = (int)(t.u / layer_div);
-        const int head = g.head_mode ? (int)(t.u % g.h) : 0;
-        const int mi0 = t.i0 + (int)crank * BM;
-        const int rowA = staged ? (int)(t.ul * g.NB) + t.pl + mi0 : layer * g.NB + t.lb + mi0;
-        const int rowB =
-            (staged ? (int)(t.ul * g.NB) + t.pm + t.j0 : layer * g.NB + t.mid + t.j0) +
-            (int)crank * BNH;
+      }
+      w = __shfl_sync(0xffffffffu, w, 0);
+      if (w < 0) break;
+      const TileInfo t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+      const int layer = (int)(t.u / layer_div);
+      const int head = g.head_mode ? (int)(t.u % g.h) : 0;
+      const int mi0 = t.i0 + (int)crank * BM;
+      if (gathered) {
+        // rows 4*lane .. 4*lane+3 of this CTA's A (left) and B (right) operand;
+        // positions past the merge's alive blocks repeat its last alive block
+        // (the epilogue masks them)
+        const int64_t gb = t.u * g.NB;
+        const int na = t.pm - t.pl, nb = t.pr - t.pm;
+        int ra[4], rb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int pa = min(mi0 + 4 * lane + q, na - 1);
+          const int pb = min(t.j0 + (int)crank * BNH + 4 * lane + q, nb - 1);
+          ra[q] = layer * (int)g.NB + live[gb + t.pl + pa];
+          rb[q] = layer * (int)g.NB + live[gb + t.pm + pb];
+        }
         for (int ks = 0; ks < nk; ++ks, ++kk) {
           const int s = kk % STAGES;
           const uint32_t ph = (kk / STAGES) & 1;
-          mbar_wait(&empty_bar[s], ph ^ 1);
-          const int dc = ks % dpc;
-          const int rest = ks / dpc;
-          const int hh = g.head_mode ? head : rest % g.h;
-          const int tok = g.head_mode ? rest : rest / g.h;
-          // pool map: (d, h, t, rows); staged map: (64, r/64, 1, rows)
-          const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
+          if (lane == 0) {
+            mbar_wait(&empty_bar[s], ph ^ 1);
+            if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+          }
+          __syncwarp();
           uint8_t* sa = smem + s * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
-          tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
-          tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
+          tma_gather4_2sm(sa + lane * 4 * BK * 2, &tmap, &full_bar[s], ks * BK, ra);
+          tma_gather4_2sm(sb + lane * 4 * BK * 2, &tmap, &full_bar[s], ks * BK, rb);
         }
+        continue;
+      }
+      if (lane != 0) continue;
+      const int rowA = staged ? (int)(t.ul * g.NB) + t.pl + mi0 : layer * g.NB + t.lb + mi0;
+      const int rowB =
+          (staged ? (int)(t.ul * g.NB) + t.pm + t.j0 : layer * g.NB + t.mid + t.j0) +
+          (int)crank * BNH;
+      for (int ks = 0; ks < nk; ++ks, ++kk) {
+        const int s = kk % STAGES;
+        const uint32_t ph = (kk / STAGES) & 1;
+        mbar_wait(&empty_bar[s], ph ^ 1);
+        const int dc = ks % dpc;
+        const int rest = ks / dpc;
+        const int hh = g.head_mode ? head : rest % g.h;
+        const int tok = g.head_mode ? rest : rest / g.h;
+        // pool map: (d, h, t, rows); staged map: (64, r/64, 1, rows)
+        const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        uint8_t* sb = sa + A_BYTES;
+        if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+        tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
+        tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
       }
     }
   } else if (warp == 1) {
@@ -561,7 +607,10 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   if (a.nt == 0 || a.nU == 0) return cudaSuccess;
   CUtensorMap tmap;
   const Geom& g = a.g;
-  const bool staged = a.live != nullptr;
+  const bool compact = a.live != nullptr;
+  const bool gathered = compact && a.staged == nullptr;  // TMA gather4 over the pool
+  const bool staged = compact && !gathered;
+  if (gathered && g.head_mode) return cudaErrorInvalidValue;
   const cuuint64_t r = (cuuint64_t)g.r();
   cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.h, (cuuint64_t)g.t,
                         (cuuint64_t)(g.L * g.NB)};
@@ -578,11 +627,20 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   }
   cuuint32_t box[4] = {(cuuint32_t)BK, 1, 1, (cuuint32_t)BM};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult res = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
-                              const_cast<void*>(staged ? a.staged : a.pool), dims, strides, box,
-                              estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult res;
+  if (gathered) {  // folded pool as 2-D (E, rows); gather4 boxes are {64, 1}
+    cuuint64_t d2[2] = {(cuuint64_t)g.E(), (cuuint64_t)(g.L * g.NB)};
+    cuuint64_t s2[1] = {(cuuint64_t)g.E() * 2};
+    cuuint32_t b2[2] = {(cuuint32_t)BK, 1};
+    res = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a.pool), d2, s2,
+                       b2, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    res = get_encode()(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4,
+                       const_cast<void*>(staged ? a.staged : a.pool), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (res != CUDA_SUCCESS) return cudaErrorInvalidValue;
   static bool attr_set = false;
   if (!attr_set) {
@@ -617,7 +675,7 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
       tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
-      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter);
+      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -144,8 +144,10 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
   a.live = live;
   a.rank = rank;
   a.staged = staged;
-  if ((live != nullptr) != (rank != nullptr) || (live != nullptr) != (staged != nullptr))
-    return fail(KVF_ERR_INVALID, "compaction needs live, rank and staged together");
+  if ((live != nullptr) != (rank != nullptr))
+    return fail(KVF_ERR_INVALID, "compaction needs live and rank together");
+  if (live && !staged && head_mode)
+    return fail(KVF_ERR_INVALID, "gathered compaction (no staged rows) needs head_mode 0");
   if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
   if (live && path != KVF_PATH_TC)
     return fail(KVF_ERR_INVALID, "compacted similarity requires the tcgen05 path");

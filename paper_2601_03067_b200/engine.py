@@ -158,7 +158,7 @@ class FusionEngine:
     """Runs fusion of all units of a geometry for one plan (see module doc)."""
 
     def __init__(self, geom: Geometry, plan: Plan, dtype: torch.dtype, device, path: int = N.PATH_AUTO,
-                 compact_from: int | None | str = "auto"):
+                 compact_from: int | None | str = "auto", compact_mode: str = "auto"):
         if plan.n_blocks != geom.NB:
             raise ConfigError(f"plan covers {plan.n_blocks} blocks, geometry has {geom.NB}")
         self.geom = geom
@@ -189,12 +189,25 @@ class FusionEngine:
         self.rescore_cap = RESCORE_CAP if path == N.PATH_TC else 0
         self.rescore = (torch.empty(4 * (self.rescore_cap + 1), dtype=torch.int32, device=dev)
                         if self.rescore_cap else None)
+        # compacted operands: "staged" (dense copy of the alive rows first, one
+        # HBM-bound kvf_stage_rows per compacted level) or "gathered" (TMA gather4
+        # of the alive rows straight from the pool, folded units; saves the staging
+        # buffer -- U*NB*r bf16 -- but measured 5x slower on the top levels of cfg2:
+        # 64 gather4 issues per k-step cannot keep up with the tensor core)
+        if compact_mode == "auto":
+            compact_mode = "staged"
+        if compact_mode not in ("gathered", "staged"):
+            raise ConfigError(f"unknown compact_mode {compact_mode!r}")
+        if compact_mode == "gathered" and geom.head_mode:
+            raise ConfigError("gathered compaction needs folded units")
+        self.compact_mode = compact_mode
         self.staged = None
         if compact_from is not None:
             self.live = torch.empty((U, NB), dtype=torch.int32, device=dev)
             self.rank = torch.empty((U, NB + 1), dtype=torch.int32, device=dev)
             self.acount = torch.empty(U, dtype=torch.int32, device=dev)
-            self.staged = torch.empty(U * NB * geom.r, dtype=torch.bfloat16, device=dev)
+            if compact_mode == "staged":
+                self.staged = torch.empty(U * NB * geom.r, dtype=torch.bfloat16, device=dev)
 
     def run(
         self,
@@ -255,9 +268,11 @@ class FusionEngine:
             if compact:
                 N.call("kvf_alive_rank", 0, U, NB, N.ptr(alive_t), N.ptr(self.live), N.ptr(self.rank),
                        N.ptr(self.acount), sp)
-                N.call("kvf_stage_rows", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(self.live),
-                       N.ptr(self.acount), N.ptr(self.staged), sp)
-                launches += 2
+                launches += 1
+                if self.staged is not None:
+                    N.call("kvf_stage_rows", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(self.live),
+                           N.ptr(self.acount), N.ptr(self.staged), sp)
+                    launches += 1
             if time_sim:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
@@ -269,7 +284,8 @@ class FusionEngine:
                 N.ptr(lv["sample_off"]) if samples is not None else None,
                 samples.shape[1] if samples is not None else 0,
                 N.ptr(self.live) if compact else None, N.ptr(self.rank) if compact else None,
-                N.ptr(self.staged) if compact else None, N.ptr(self.rescore), self.rescore_cap,
+                N.ptr(self.staged) if compact and self.staged is not None else None,
+                N.ptr(self.rescore), self.rescore_cap,
                 RESCORE_BAND if self.rescore_cap else 0.0, self.path, sp,
             )
             if self.rescore_cap:

@@ -65,21 +65,26 @@ def test_tc_matches_simt_and_oracle(shape, head_mode):
         np.testing.assert_array_equal(st_tc.refcount[u].cpu().numpy(), ref.refcount)
 
 
-@pytest.mark.parametrize("shape,head_mode,compact_from", [
-    ((2, 16, 32, 16, 8, 128), 0, 1),   # every level compacted
-    ((1, 16, 40, 16, 8, 128), 0, 3),   # top levels only, partial tiles
-    ((1, 16, 24, 16, 2, 128), 1, 2),   # per-head units
+@pytest.mark.parametrize("shape,head_mode,compact_from,mode", [
+    ((2, 16, 32, 16, 8, 128), 0, 1, "staged"),    # every level compacted
+    ((2, 16, 32, 16, 8, 128), 0, 1, "gathered"),  # ... operands via TMA gather4
+    ((1, 16, 40, 16, 8, 128), 0, 3, "staged"),    # top levels only, partial tiles
+    ((1, 16, 40, 16, 8, 128), 0, 3, "gathered"),
+    ((1, 13, 37, 16, 4, 64), 0, 1, "gathered"),   # odd sizes, d = 64
+    ((1, 16, 24, 16, 2, 128), 1, 2, "staged"),    # per-head units
 ])
-def test_tc_compaction_bitwise(shape, head_mode, compact_from):
-    """Compacted levels (staged alive rows) must reproduce the direct kernel's
-    similarities bit for bit, hence identical decisions, tables and pools."""
+def test_tc_compaction_bitwise(shape, head_mode, compact_from, mode):
+    """Compacted levels (alive rows staged densely, or gathered from the pool
+    with TMA gather4) must reproduce the direct kernel's similarities bit for
+    bit, hence identical decisions, tables and pools."""
     L, B, p, t, h, d = shape
     Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=9)
     geom = K.Geometry(L, B * p, t, h, d, head_mode)
     plan = bff_plan(B, p, None)
     outs = []
     for cf in (None, compact_from):
-        eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, compact_from=cf)
+        eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, compact_from=cf,
+                           compact_mode=mode)
         assert eng.compact_from == cf
         outs.append(eng.run(Kt.clone().reshape(-1), Vt.clone().reshape(-1), 0.8, keep_samples=True))
     a, b = outs
