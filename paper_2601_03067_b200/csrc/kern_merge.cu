@@ -494,6 +494,93 @@ merge_reg_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4 for short vectors (per-head units, r * sizeof(T) <= 4 KB): one warp per
+// (absorber, K|V) item, CPL 16-byte chunks per lane in registers, warp-tree
+// norms. Many items in flight per SM instead of one block-wide reduction per
+// 4 KB vector.
+// ---------------------------------------------------------------------------
+template <typename T, int VEC, int CPL>
+__global__ void __launch_bounds__(256, 2)
+merge_warp_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
+                  float* __restrict__ knorm, float* __restrict__ vnorm,
+                  const float* __restrict__ oknorm, const float* __restrict__ ovnorm,
+                  int32_t* ws, int64_t n_total) {
+  const LevelWs W(ws, n_total);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_items = 2 * (int64_t)(*W.count);
+  for (int64_t it = warp; it < n_items; it += nwarps) {
+    const bool is_v = it & 1;
+    T* pool = is_v ? pool_v : pool_k;
+    float* norm = is_v ? vnorm : knorm;
+    const int64_t gid = W.list[it >> 1];
+    const int64_t u = gid / g.NB;
+    const int64_t gb = u * g.NB;
+    const int32_t l = (int32_t)(gid % g.NB);
+    const int n = W.mcnt[gid], s0 = W.mstart[gid];
+    // lane k holds vector k's id and 1/norm (k = 0: the absorber itself)
+    int32_t id_l = l;
+    float inv_l = 0.f;
+    if (lane <= n) {
+      if (lane > 0) id_l = W.members[s0 + lane - 1];
+      const float nv = norm[gb + id_l];
+      inv_l = nv > 0.f ? 1.f / nv : 0.f;
+    }
+    float acc[CPL][VEC];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc[q][e] = 0.f;
+    for (int v = 0; v <= n; ++v) {
+      int32_t id;
+      float inv;
+      if (v < 32) {
+        id = __shfl_sync(0xffffffffu, id_l, v);
+        inv = __shfl_sync(0xffffffffu, inv_l, v);
+      } else {  // groups beyond one warp of members
+        id = W.members[s0 + v - 1];
+        const float nv = norm[gb + id];
+        inv = nv > 0.f ? 1.f / nv : 0.f;
+      }
+      const T* x = pool + g.base(u, id);
+      uint4 raw[CPL];  // 16-byte chunks kept packed until use (register budget)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+        raw[q] = __ldg(reinterpret_cast<const uint4*>(x + g.off((int64_t)(q * 32 + lane) * VEC)));
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        float y[VEC];
+        VecIO<T, VEC>::load(reinterpret_cast<const T*>(&raw[q]), y);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[q][e] = fmaf(y[e], inv, acc[q][e]);
+      }
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) ss = fmaf(acc[q][e], acc[q][e], ss);
+    const float nrm = sqrtf(warp_sum(ss));
+    const float home = (is_v ? ovnorm : oknorm)[gid];
+    const float sc = nrm > 0.f ? (home > 0.f ? home : 1.f) / nrm : 0.f;
+    T* xl = pool + g.base(u, l);
+    float rs = 0.f;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      float yv[VEC], rd[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) yv[e] = acc[q][e] * sc;
+      VecIO<T, VEC>::store(xl + g.off((int64_t)(q * 32 + lane) * VEC), yv, rd);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) rs = fmaf(rd[e], rd[e], rs);
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) norm[gid] = sqrtf(rs);
+  }
+}
+
 namespace {
 template <typename T, int VEC>
 cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
@@ -539,6 +626,20 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
   if constexpr (!std::is_same<T, double>::value) {
+    // short vectors (per-head units): warp per item
+    const bool vec_ok = can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g);
+    if (vec_ok && vbytes <= 4096 && r % (32 * VEC) == 0) {
+      const int cpl = (int)(r / (32 * VEC));
+      auto launch = [&](auto kern) {
+        kern<<<148 * 8, 256, 0, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn, (const float*)okn,
+                                     (const float*)ovn, ws, n_total);
+        return cudaGetLastError();
+      };
+      if (cpl == 1) return launch(merge_warp_kernel<T, VEC, 1>);
+      if (cpl == 2) return launch(merge_warp_kernel<T, VEC, 2>);
+      if (cpl == 4) return launch(merge_warp_kernel<T, VEC, 4>);
+      if (cpl == 8) return launch(merge_warp_kernel<T, VEC, 8>);
+    }
     if (tma_ok) {
       const int64_t ept = (r + MG_CONSUMERS - 1) / MG_CONSUMERS;
       if (ept <= 8)
