@@ -536,8 +536,9 @@ template <int D, int T>
 cudaError_t decode_sched_ib(const DecodeArgs& a, cudaStream_t s) {
   // one block per warp tile; 16-token blocks: 8 KB stages, 12 warps x 2 stages.
   // Measured on B200 at batch 64 x 4K (us per layer): 8 warps x 3 stages 143.6,
-  // 12 x 2 121.8, 14 x 2 122.8; two blocks per tile: 6 x 2 141.0, 4 x 3 164.4
-  // (the warp loop is latency bound: warps per SM beat deeper rings and tiles).
+  // 12 x 2 121.8, 13 x 2 138.1, 14 x 2 122.8, 9 x 3 152.0, 7 x 4 139.1; two blocks
+  // per tile: 6 x 2 141.0, 4 x 3 164.4 (the warp loop is latency bound: warps per
+  // SM -- balanced over the 4 schedulers -- beat deeper rings and larger tiles).
   constexpr int DW = T == 16 ? 12 : 6;
   if (a.sched->ib == 16) return decode_sched_t<D, T, 1, DW, 2, 16>(a, s);
   if (a.sched->ib == 8) return decode_sched_t<D, T, 1, DW, 2, 8>(a, s);
