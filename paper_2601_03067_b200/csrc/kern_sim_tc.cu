@@ -15,7 +15,8 @@
 //               per 64-wide k-step; tcgen05.commit multicasts the stage
 //               release to both CTAs
 //   warp 2      TMEM allocator (2 x 256 columns, cta_group::2)
-//   warps 4..7  epilogue: per-tile column metadata, tcgen05.ld 32x32b.x32
+//   warps 4..11 epilogue (two warps per TMEM lane quarter, one per column
+//               half): per-tile column metadata, tcgen05.ld 32x32b.x32
 //               -> sim = acc / (|x_i||x_j|), alive/fusable masks, strict
 //               '> thr' (pairs within resc_band deferred to the exact
 //               re-score), per-column min row via redux.sync + smem atomicMin
@@ -41,8 +42,9 @@ constexpr int A_BYTES = BM * BK * 2;   // 16 KB
 constexpr int B_BYTES = BNH * BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;  // two 256-column accumulators
-constexpr int NTHREADS = 256;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 4096 /*meta*/;
+constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quarter, each half of the columns
+constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*meta*/;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // cluster smem address of CTA 0
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -202,9 +204,9 @@ __device__ __forceinline__ void st_cluster_s32(const void* p, uint32_t cta, int3
 }
 
 constexpr int SCHED_DEPTH = 4;
-// sched_empty arrivals per slot: leader MMA warp + peer producer + 4 epilogue
+// sched_empty arrivals per slot: leader MMA warp + peer producer + EPI_WARPS epilogue
 // warps in each CTA
-constexpr uint32_t kSchedConsumers = 10;
+constexpr uint32_t kSchedConsumers = 2 + 2 * EPI_WARPS;
 
 // Persistent: P CTA pairs pull work items from a global counter (the leader's
 // producer thread fetches, skips tiles beyond the alive blocks, and broadcasts
@@ -235,8 +237,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   float* inv_j = reinterpret_cast<float*>(meta + 512);
   int32_t* colmin = reinterpret_cast<int32_t*>(meta + 512 + 4 * BN);
   uint8_t* ok_j = meta + 512 + 8 * BN;
-  double* red = reinterpret_cast<double*>(meta + 512 + 9 * BN);            // 4 warps x 5
-  int32_t* colid = reinterpret_cast<int32_t*>(meta + 512 + 9 * BN + 256);  // block ids
+  double* red = reinterpret_cast<double*>(meta + 512 + 9 * BN);            // 8 warps x 5
+  int32_t* colid = reinterpret_cast<int32_t*>(meta + 512 + 9 * BN + 512);  // block ids
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
@@ -255,7 +257,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
-      mbar_init(&tmem_empty[b], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tmem_empty[b], 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
     }
     for (int b = 0; b < SCHED_DEPTH; ++b) {
       mbar_init(&sched_full[b], 1);
@@ -402,9 +404,12 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       }
     }
   } else if (warp >= 4) {
-    const int ew = warp - 4;  // TMEM lanes [32*ew, 32*ew + 32)
-    const int row = ew * 32 + lane;
+    const int ew = warp - 4;
+    const int quarter = ew & 3;           // TMEM lanes [32*quarter, 32*quarter + 32)
+    const int col0 = (ew >> 2) * (BN / 2);  // this warp's half of the columns
+    const int row = quarter * 32 + lane;
     const int et = threadIdx.x - 128;
+    constexpr int ET = 32 * EPI_WARPS;
     uint32_t tc = 0;
     for (uint32_t it = 0;; ++it) {
       const int sl = it % SCHED_DEPTH;
@@ -421,7 +426,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int mi0 = t.i0 + (int)crank * BM;
       const int ni = max(0, min(BM, t.pm - t.pl - mi0));  // valid rows of this CTA
       const int nj = min(BN, t.pr - t.pm - t.j0);
-      for (int c = et; c < BN; c += 128) {  // column metadata
+      for (int c = et; c < BN; c += ET) {  // column metadata
         const int64_t bj = gb + (c < nj ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
         const bool ok = c < nj && alive[bj] && fusable[bj];
         colid[c] = (int32_t)(bj - gb);
@@ -437,52 +442,59 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const float inv_i = ni_v > 0.f ? 1.f / ni_v : 0.f;
       float cnt = 0.f, s1 = 0.f, s2 = 0.f, mn = INFINITY, mx = -INFINITY;
       double* samp = samples ? samples + t.ul * sample_stride + sample_off[t.m] : nullptr;
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // column metadata visible
+      asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");  // column metadata visible
 
       const uint32_t acc = tc & 1;
       mbar_wait(&tmem_full[acc], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      // pairs with s > tlo take the slow path: threshold decision, or deferral
+      // of near-threshold pairs to the exact float64 re-score (the tensor-core
+      // fp32 accumulation over r/16 steps can be off by ~1e-4 relative)
+      const float tlo = resc != nullptr ? thr - resc_band : thr;
+      for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + c0, v);
-        int32_t mine = kNone;
+        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
+        // columns of this chunk that take part (alive, fusable, inside the merge)
+        const unsigned okm = __ballot_sync(0xffffffffu, ok_j[c0 + lane] != 0);
+        if (ok_i) cnt += (float)__popc(okm);
+        unsigned hitm = 0;  // lane c: rows of this warp with a decided match in column c0 + c
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
           const int col = c0 + c;
-          const bool ok = ok_i && ok_j[col];
+          const bool ok = ok_i && ((okm >> c) & 1u);
           const float s = __uint_as_float(v[c]) * inv_i * inv_j[col];
-          int32_t cand = kNone;
+          bool hit = false;
           if (ok) {
-            cnt += 1.f;
             s1 += s;
-            s2 += s * s;
+            s2 = fmaf(s, s, s2);
             mn = fminf(mn, s);
             mx = fmaxf(mx, s);
-            // The tensor-core fp32 accumulation over r/16 steps can be off by
-            // ~1e-4 relative: pairs that close to the threshold are deferred to
-            // an exact float64 re-score (kvf_rescore) instead of decided here.
-            bool decided = true;
-            if (resc != nullptr && fabsf(s - thr) <= resc_band) {
-              const int pos = atomicAdd(resc_count, 1);
-              if (pos < resc_cap) {
-                int4 e;
-                e.x = (int)t.u;
-                e.y = my_id;
-                e.z = colid[col];
-                e.w = t.m;
-                reinterpret_cast<int4*>(resc)[pos] = e;
-                decided = false;
+            if (s > tlo) {
+              hit = s > thr;
+              if (resc != nullptr && fabsf(s - thr) <= resc_band) {
+                const int pos = atomicAdd(resc_count, 1);
+                if (pos < resc_cap) {
+                  int4 e;
+                  e.x = (int)t.u;
+                  e.y = my_id;
+                  e.z = colid[col];
+                  e.w = t.m;
+                  reinterpret_cast<int4*>(resc)[pos] = e;
+                  hit = false;  // decided by the re-score
+                }
               }
             }
-            if (decided && s > thr) cand = my_id;
           }
           if (samp && row < ni && col < nj)
             samp[(int64_t)(my_id - t.lb) * (t.re - t.mid) + (colid[col] - t.mid)] =
                 ok ? (double)s : (double)NAN;
-          const int32_t wmin = (int32_t)__reduce_min_sync(0xffffffffu, (uint32_t)cand);
-          if (lane == c) mine = wmin;
+          const unsigned b = __ballot_sync(0xffffffffu, hit);
+          if (lane == c) hitm = b;
         }
-        if (mine != kNone) atomicMin(&colmin[c0 + lane], mine);
+        // first matching row of the warp per column (rows ascend with block id)
+        const int src = hitm ? __ffs(hitm) - 1 : 0;
+        const int32_t first = __shfl_sync(0xffffffffu, my_id, src);
+        if (hitm) atomicMin(&colmin[c0 + lane], first);
       }
       // accumulator drained: hand the buffer back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -506,14 +518,14 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         red[ew * 5 + 3] = dmn;
         red[ew * 5 + 4] = dmx;
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int c = et; c < BN; c += 128) {
+      asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");
+      for (int c = et; c < BN; c += ET) {
         const int32_t cm = colmin[c];
         if (cm != kNone) atomicMin(&absorber[gb + colid[c]], cm);
       }
       if (et == 0) {
         double o[5] = {0, 0, 0, INFINITY, -INFINITY};
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < EPI_WARPS; ++q) {
           o[0] += red[q * 5 + 0];
           o[1] += red[q * 5 + 1];
           o[2] += red[q * 5 + 2];
@@ -522,7 +534,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         }
         for (int q = 0; q < 5; ++q) pp[q] = o[q];
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // metadata free for the next tile
+      asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");  // metadata free for the next tile
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
