@@ -209,6 +209,12 @@ class FusionEngine:
             if compact_mode == "staged":
                 self.staged = torch.empty(U * NB * geom.r, dtype=torch.bfloat16, device=dev)
 
+    def capture(self, pool_k: torch.Tensor, pool_v: torch.Tensor, threshold: float, *,
+                keep_samples: bool = False) -> "CapturedFusion":
+        """Capture run(pool_k, pool_v, threshold) as a CUDA graph (see CapturedFusion).
+        The capture itself runs the fusion twice on the pools (warm-up, capture)."""
+        return _capture(self, pool_k, pool_v, threshold, keep_samples)
+
     def run(
         self,
         pool_k: torch.Tensor,
@@ -324,6 +330,40 @@ class FusionEngine:
         launches += 2
         st.launches = launches
         return st
+
+
+class CapturedFusion:
+    """A fusion run captured as one CUDA graph (FusionEngine.capture).
+
+    replay() re-runs every launch of the captured run -- norms, all tree
+    levels, finalize -- on the same pool buffers with one host call, removing
+    the per-launch host overhead that dominates small caches (CFF chunks).
+    The pools are fused in place by every replay, so callers restore them
+    first when they need the pristine cache; `state` holds the run's static
+    output tensors, overwritten by each replay.
+    """
+
+    def __init__(self, graph: torch.cuda.CUDAGraph, state: "FusionState", stream):
+        self.graph = graph
+        self.state = state
+        self.stream = stream
+
+    def replay(self) -> "FusionState":
+        self.graph.replay()
+        return self.state
+
+
+def _capture(engine: "FusionEngine", pool_k, pool_v, threshold, keep_samples=False) -> CapturedFusion:
+    s = torch.cuda.Stream(engine.device)
+    s.wait_stream(torch.cuda.current_stream(engine.device))
+    with torch.cuda.stream(s):  # warm-up on the capture stream: per-stream scheduler state,
+        engine.run(pool_k, pool_v, threshold, keep_samples=keep_samples)  # kernel attributes
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        st = engine.run(pool_k, pool_v, threshold, keep_samples=keep_samples)
+    torch.cuda.current_stream(engine.device).wait_stream(s)
+    return CapturedFusion(g, st, s)
 
 
 def tc_available(geom: Geometry) -> bool:
