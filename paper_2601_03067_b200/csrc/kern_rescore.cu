@@ -10,24 +10,29 @@
 
 namespace kvf {
 
+// One CTA per queued pair (the queue is short -- tens to hundreds of pairs per
+// level -- so per-pair latency, not throughput, bounds the launch): 256
+// threads split the r-element dot products, float64 accumulation (bf16 and
+// fp32 products are exact in float64), fixed-order block reduction.
 template <typename T, int VEC>
-__global__ void rescore_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
-                               const int4* __restrict__ list, const int32_t* __restrict__ count,
-                               int64_t cap, double thr, int32_t* absorber,
-                               const int32_t* __restrict__ merges, double* samples,
-                               const int64_t* __restrict__ sample_off, int64_t sample_stride) {
+__global__ void __launch_bounds__(256)
+rescore_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
+               const int4* __restrict__ list, const int32_t* __restrict__ count,
+               int64_t cap, double thr, int32_t* absorber,
+               const int32_t* __restrict__ merges, double* samples,
+               const int64_t* __restrict__ sample_off, int64_t sample_stride) {
   using A = typename AccOf<T>::type;
-  const int lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  __shared__ double red[3][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = min((int64_t)*count, cap);
   const int64_t nch = g.r() / VEC;
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < n; w += nw) {
+  for (int64_t w = blockIdx.x; w < n; w += gridDim.x) {
     const int4 e = list[w];
     const int64_t u = e.x;
     const T* x = pool + g.base(u, e.y);
     const T* y = pool + g.base(u, e.z);
     double dxy = 0.0, dxx = 0.0, dyy = 0.0;
-    for (int64_t c = lane; c < nch; c += 32) {
+    for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) {
       A a[VEC], b[VEC];
       VecIO<T, VEC>::load_nc(x + g.off(c * VEC), a);
       VecIO<T, VEC>::load_nc(y + g.off(c * VEC), b);
@@ -43,7 +48,19 @@ __global__ void rescore_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
     dxx = warp_sum(dxx);
     dyy = warp_sum(dyy);
     if (lane == 0) {
-      const double s = (dxx > 0.0 && dyy > 0.0) ? dxy / sqrt(dxx * dyy) : 0.0;
+      red[0][warp] = dxy;
+      red[1][warp] = dxx;
+      red[2][warp] = dyy;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sxy = 0.0, sxx = 0.0, syy = 0.0;
+      for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+        sxy += red[0][q];
+        sxx += red[1][q];
+        syy += red[2][q];
+      }
+      const double s = (sxx > 0.0 && syy > 0.0) ? sxy / sqrt(sxx * syy) : 0.0;
       if (s > thr) atomicMin(&absorber[u * g.NB + e.z], e.y);
       if (samples) {
         const int lb = merges[3 * e.w], mid = merges[3 * e.w + 1], re = merges[3 * e.w + 2];
@@ -51,12 +68,13 @@ __global__ void rescore_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
                 (e.z - mid)] = s;
       }
     }
+    __syncthreads();
   }
 }
 
 template <typename T>
 static cudaError_t rescore_t(const RescoreArgs& a, cudaStream_t s) {
-  const int grid = 148 * 4;
+  const int grid = 148 * 8;
   if (can_vectorize<T>(a.pool, a.g))
     rescore_kernel<T, Vec16<T>::N><<<grid, 256, 0, s>>>(
         (const T*)a.pool, a.g, a.u0, (const int4*)a.resc, a.resc_count, a.resc_cap, a.thr,
