@@ -15,6 +15,7 @@
 //   eight consumer warps accumulating in registers (fp32) -> HBM-bound.
 //   Fallback (fp64 pools, unaligned pools): register-only CTA per item.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 #include "kernels.h"
 #include "vec_io.cuh"
@@ -250,7 +251,7 @@ struct SlotMeta {
 };
 
 template <typename T, int EPT>
-__global__ void __launch_bounds__(MG_THREADS, 1)
+__global__ void __launch_bounds__(MG_THREADS, 2)
 merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* __restrict__ knorm,
                  float* __restrict__ vnorm, const float* __restrict__ oknorm,
                  const float* __restrict__ ovnorm, int32_t* ws, int64_t n_total, int nbuf,
@@ -608,7 +609,21 @@ cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, con
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  merge_tma_kernel<T, EPT><<<148, MG_THREADS, smem, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn,
+  // two CTAs per SM: one CTA's per-item tail (norm reduction, write-back,
+  // stored-norm reduction) overlaps the other's streaming. Measured on 4 cfg2
+  // layers (6 levels): 1 CTA x 6 slots 4.98 ms, 2 x 3 slots 3.47 ms, 3 x 2 4.33 ms.
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  static const int per_sm = [] {  // tuning knob for A/B measurements
+    const char* e = getenv("KVF_MERGE_CTAS_PER_SM");
+    return e ? std::max(1, atoi(e)) : 2;
+  }();
+  merge_tma_kernel<T, EPT><<<per_sm * n_sm, MG_THREADS, smem, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn,
                                                          (const float*)okn, (const float*)ovn, ws,
                                                          n_total, nbuf, slot_bytes);
   return cudaGetLastError();
@@ -621,7 +636,9 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
   const int64_t r = g.r();
   const int64_t vbytes = r * (int64_t)sizeof(T);
   const int slot_bytes = (int)((vbytes + 127) / 128 * 128);
-  const int nbuf = (int)std::min<int64_t>(MG_MAX_BUF, (200 * 1024) / slot_bytes);
+  const char* ev = getenv("KVF_MERGE_CTAS_PER_SM");
+  const int per_sm = ev ? std::max(1, atoi(ev)) : 2;
+  const int nbuf = (int)std::min<int64_t>(MG_MAX_BUF, (200 * 1024 / per_sm) / slot_bytes);
   const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
