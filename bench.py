@@ -259,7 +259,7 @@ def run_cpu_decode_sample():
 
 def run_cpu_sample(config, steps, warmup, seed=7):
     cores = os.cpu_count() or 1
-    layers = max(1, min(cores, 8))
+    layers = max(1, min(cores, 16))  # one layer per host thread (KVFUSE_THREADS), all cores
     env = dict(os.environ)
     env.update(OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1",
                KVFUSE_THREADS=str(layers))
