@@ -208,6 +208,18 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
                      void* out, void* lse, void* probs, void* workspace,
                      int64_t workspace_bytes, void* stream);
 
+/* Percentile mode of the threshold controller on the device (fusion.py:418-437,
+ * SURVEY §8f rank 3): *out = np.quantile(x, q) (numpy's default 'linear'
+ * method) over the non-NaN entries of nparts float64 device segments
+ * parts[i][0:lens[i]] (host arrays of device pointers / lengths; e.g. the
+ * per-level sample rows of a fusion run, masked pairs are NaN). NaN when no
+ * sample is valid. Exact: 8-pass radix select on order-preserving keys.
+ * workspace: kvf_quantile_ws_bytes() device bytes. */
+int64_t kvf_quantile_ws_bytes(void);
+int kvf_quantile(const void* const* parts, const int64_t* lens, int nparts,
+                 double q, double* out, void* workspace,
+                 int64_t workspace_bytes, void* stream);
+
 /* Compaction of a fused layer (the reference's FusedCache storage: live
  * blocks only, ascending physical id, core.py:246-270 / fusion.py:318-327):
  * kvf_alive_rank gives the ascending live ids and the exclusive alive rank of

@@ -121,6 +121,11 @@ cudaError_t launch_refold(const void* pool, int dtype, const Geom& g, int64_t la
                           cudaStream_t s);
 
 struct SchedView;
+// exact np.quantile (linear) of the non-NaN entries of float64 device segments
+int64_t quantile_ws_bytes();
+cudaError_t launch_quantile(const void* const* parts, const int64_t* lens, int nseg, double q,
+                            double* out, void* ws, cudaStream_t s);
+
 int64_t decode_workspace_size(int dtype, int64_t B, int Hq, int d, int64_t p_blocks, int t);
 struct DecodeArgs {
   const void* q;

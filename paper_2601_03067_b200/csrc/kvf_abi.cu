@@ -372,6 +372,20 @@ int kvf_remap_ids(const int32_t* ids, int64_t n, const int32_t* map, int64_t map
                      "kvf_remap_ids");
 }
 
+int64_t kvf_quantile_ws_bytes(void) { return quantile_ws_bytes(); }
+
+int kvf_quantile(const void* const* parts, const int64_t* lens, int nparts, double q, double* out,
+                 void* workspace, int64_t workspace_bytes, void* stream) {
+  if (!(q >= 0.0 && q <= 1.0)) return fail(KVF_ERR_INVALID, "quantile q must lie in [0, 1], got %g", q);
+  if (nparts < 0 || (nparts > 0 && (!parts || !lens))) return fail(KVF_ERR_INVALID, "bad segment list");
+  if (!out || !workspace) return fail(KVF_ERR_INVALID, "null pointer");
+  if (workspace_bytes < quantile_ws_bytes()) return fail(KVF_ERR_INVALID, "quantile workspace too small");
+  for (int i = 0; i < nparts; ++i)
+    if (lens[i] < 0 || (lens[i] > 0 && !parts[i])) return fail(KVF_ERR_INVALID, "bad segment %d", i);
+  return cuda_status(launch_quantile(parts, lens, nparts, q, out, workspace, (cudaStream_t)stream),
+                     "kvf_quantile");
+}
+
 int kvf_decode_schedule_item_blocks(void) { return 16; }
 
 int64_t kvf_decode_schedule_ws_ints(int head_mode, int h, int64_t NB, int64_t B, int64_t p_blocks,

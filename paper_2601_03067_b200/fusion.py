@@ -199,6 +199,14 @@ class FusionReport:
     def similarity_samples(self, v):
         self._samples = v
 
+    def device_samples(self) -> list | None:
+        """Device sample rows (float64, NaN = masked pair) when the samples were
+        kept on the GPU and not yet copied to the host, else None."""
+        if self._samples is not None or self._lazy is None:
+            return None
+        fn = getattr(self._lazy, "device_samples", None)
+        return fn() if fn is not None else None
+
     @property
     def samples_materialized(self) -> bool:
         return self._lazy is None or self._lazy.has_samples
@@ -259,8 +267,12 @@ class FusionReport:
     @classmethod
     def aggregate(cls, reports: list["FusionReport"]) -> "FusionReport":
         """Collapse per-unit reports into one with layer -1 (fusion.py:158-171)."""
+        parts = [r.device_samples() for r in reports]
+        on_device = bool(reports) and all(p is not None for p in parts)
         all_mat = all(r.samples_materialized for r in reports)
-        if all_mat:
+        if on_device:  # keep them on the GPU; the host copy is built on first access
+            samp = None
+        elif all_mat:
             samples = [r.similarity_samples for r in reports if r.similarity_samples.size]
             samp = np.concatenate(samples) if samples else np.empty(0)
         else:
@@ -273,11 +285,34 @@ class FusionReport:
             merge_calls=sum(r.merge_calls for r in reports),
             tree_depth=max((r.tree_depth for r in reports), default=0),
             similarity_samples=samp,
-            merge_records=[m for r in reports for m in r.merge_records],
+            merge_records=None if on_device else [m for r in reports for m in r.merge_records],
         )
-        if samp is None:
+        if on_device:
+            out._lazy = _DeviceParts([t for p in parts for t in p], reports)
+        elif samp is None:
             out._lazy = _NoSamples()
         return out
+
+
+class _DeviceParts:
+    """Aggregate of reports whose samples are still on the device."""
+
+    has_samples = True
+
+    def __init__(self, parts, reports):
+        self.parts = parts
+        self.reports = reports
+
+    def device_samples(self):
+        return self.parts
+
+    def records(self):
+        return [m for r in self.reports for m in r.merge_records]
+
+    def samples(self):  # host copy in the reference's order (report, merge post-order)
+        arrs = [r.similarity_samples for r in self.reports]
+        arrs = [a for a in arrs if a.size]
+        return np.concatenate(arrs) if arrs else np.empty(0)
 
 
 class _NoSamples:
@@ -417,6 +452,12 @@ class _UnitLazy:
                 MergeRecord(hgt, s[0], s[1], samples, s[2], moments=(s[3], s[4], s[5], s[6], s[7]))
             )
         return recs
+
+    def device_samples(self) -> list | None:
+        if not self.has_samples:
+            return None
+        st = self.run.st
+        return [smp[self.unit] for smp in st.level_samples if smp is not None]
 
     def samples(self) -> np.ndarray:
         if not self.has_samples:
@@ -662,6 +703,28 @@ def fast_fusion(keys: UnfoldedLayer, values: UnfoldedLayer, thr: float,
     return _outcomes_from_state(st, ks, rows, bpr, shape, tables=tables, layer_override=layer)[0]
 
 
+def device_quantile(parts: list[torch.Tensor], q: float) -> float:
+    """np.quantile(concat(non-NaN entries of parts), q) computed on the GPU
+    (kvf_quantile: exact radix select, numpy's 'linear' interpolation)."""
+    import ctypes as C
+
+    parts = [t for t in parts if t is not None and t.numel()]
+    if parts and any(t.dtype != torch.float64 or not t.is_cuda for t in parts):
+        raise ConfigError("device_quantile takes float64 CUDA tensors")
+    dev = parts[0].device if parts else torch.device("cuda")
+    parts = [t.contiguous() for t in parts]
+    ptrs = (C.c_void_p * max(len(parts), 1))(*[t.data_ptr() for t in parts])
+    lens = (C.c_int64 * max(len(parts), 1))(*[t.numel() for t in parts])
+    ws = torch.empty(int(N.lib().kvf_quantile_ws_bytes()), dtype=torch.uint8, device=dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    N.call("kvf_quantile", ptrs, lens, len(parts), float(q), N.ptr(out), N.ptr(ws), ws.numel(),
+           N.stream_ptr())
+    v = float(out.item())
+    if math.isnan(v):
+        raise InsufficientDataError("percentile adaptation needs a nonempty similarity sample set")
+    return v
+
+
 def adapt_threshold(policy: AdaptPolicy, report: FusionReport, current: float) -> float:
     """One step of the threshold controller (fusion.py:418-437)."""
     if policy.mode == "target-compression":
@@ -671,10 +734,14 @@ def adapt_threshold(policy: AdaptPolicy, report: FusionReport, current: float) -
         if cr < policy.target:
             return max(current - policy.step, policy.min_threshold)
         return current
-    samples = report.similarity_samples
-    if samples.size == 0:
-        raise InsufficientDataError("percentile adaptation needs a nonempty similarity sample set")
-    q = float(np.quantile(samples, 1.0 - policy.target))
+    dev = report.device_samples()
+    if dev is not None:  # samples still on the GPU: exact quantile without a host copy
+        q = device_quantile(dev, 1.0 - policy.target)
+    else:
+        samples = report.similarity_samples
+        if samples.size == 0:
+            raise InsufficientDataError("percentile adaptation needs a nonempty similarity sample set")
+        q = float(np.quantile(samples, 1.0 - policy.target))
     return min(max(q, policy.min_threshold), policy.max_threshold)
 
 

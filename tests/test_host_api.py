@@ -111,3 +111,42 @@ def test_reports_json_csv_aggregate_match_reference():
     for r, want in zip(reports, host["json"]):
         _close(json.loads(r.to_json()), json.loads(want))
     _close(FusionReport.aggregate(reports).to_dict(), host["aggregate"])
+
+
+@pytest.mark.gpu
+def test_device_quantile_matches_numpy():
+    import torch
+
+    from paper_2601_03067_b200.fusion import device_quantile
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    for n, nan_frac in ((1, 0.0), (2, 0.0), (7, 0.3), (1000, 0.5), (100_003, 0.1)):
+        x = torch.randn(n, generator=g, device="cuda", dtype=torch.float64)
+        x[torch.rand(n, generator=g, device="cuda") < nan_frac] = float("nan")
+        x[: n // 3] = torch.round(x[: n // 3] * 4) / 4  # ties
+        if n > 1:
+            x[0] = -0.0
+        parts = [x[: n // 2], x[n // 2:]]
+        h = x.cpu().numpy()
+        h = h[~np.isnan(h)]
+        for q in (0.0, 0.2, 0.5, 0.8, 0.93, 1.0):
+            if h.size == 0:
+                continue
+            assert device_quantile(parts, q) == np.quantile(h, q), (n, q)
+    with pytest.raises(InsufficientDataError):
+        device_quantile([torch.full((5,), float("nan"), dtype=torch.float64, device="cuda")], 0.5)
+
+
+@pytest.mark.gpu
+def test_percentile_adaptation_on_device_samples():
+    """Percentile mode over a fused cache's device samples equals the host path."""
+    reports = [o.report for o in K.fuse_batch(_clusters4(), FusionConfig(threshold=0.91), keep_samples=True)]
+    pol = AdaptPolicy(mode="percentile", target=0.2, step=0.01, min_threshold=0.0, max_threshold=0.99)
+    agg = FusionReport.aggregate(reports)
+    assert agg.device_samples() is not None
+    dev = adapt_threshold(pol, agg, 0.5)
+    for r in reports:
+        r.similarity_samples  # materialise on the host -> host path
+    host = adapt_threshold(pol, FusionReport.aggregate(reports), 0.5)
+    want = float(np.quantile(np.concatenate([r.similarity_samples for r in reports]), 0.8))
+    assert dev == host == want
