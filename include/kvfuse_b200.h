@@ -242,6 +242,9 @@ int kvf_remap_ids(const int32_t* ids, int64_t n, const int32_t* map,
  *   phys  int32 [nh][B*nit][item_blocks] physical block of each item slot
  *                                  (-1 = padding); ks / vs float, same shape:
  *                                  the slots' K / V scales
+ * n_repeats (optional, int32[1]): slots that repeat the previous slot's block
+ * inside an item (runs of a block the request references several times, e.g.
+ * after CFF); nonzero -> pass dedup = 1 to kvf_paged_decode_sched.
  * item_blocks: 8 or 16 (kvf_decode_schedule_item_blocks() = tuned default).
  * workspace: kvf_decode_schedule_ws_ints() int32 words. Rebuild the schedule
  * after any change of the layer's table or scales. */
@@ -254,10 +257,13 @@ int kvf_decode_schedule(const int32_t* table, const void* k_scale,
                         int64_t p_blocks, const int32_t* seq_blocks,
                         int item_blocks, int32_t* order, int32_t* meta,
                         int32_t* phys, float* ks, float* vs, int32_t* n_items,
-                        int32_t* workspace, int64_t workspace_ints,
-                        void* stream);
+                        int32_t* n_repeats, int32_t* workspace,
+                        int64_t workspace_ints, void* stream);
 /* K6 over a schedule: persistent warps sweep the items head by head, so
- * requests sharing a fused block read it within one L2 window. bf16 pools,
+ * requests sharing a fused block read it within one L2 window; with dedup, a
+ * run of slots on one block is loaded once, S = K q^T is computed once and
+ * reused with each slot's scale, and P V runs once on the scale-weighted sum
+ * of the run's probabilities (computation reuse). bf16 pools,
  * d in {64, 128}, t | 32. Same q / out / lse contract as kvf_paged_decode
  * (no probability output); workspace >= B*Hq*nit*(d+2)*4 bytes. */
 int kvf_paged_decode_sched(const void* q, int q_dtype, const void* pool_k,
@@ -269,7 +275,7 @@ int kvf_paged_decode_sched(const void* q, int q_dtype, const void* pool_k,
                            double sm_scale, void* out, void* lse,
                            int item_blocks, const int32_t* meta,
                            const int32_t* phys, const float* ks,
-                           const float* vs, const int32_t* n_items,
+                           const float* vs, const int32_t* n_items, int dedup,
                            void* workspace, int64_t workspace_bytes,
                            void* stream);
 

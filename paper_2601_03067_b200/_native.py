@@ -90,12 +90,13 @@ SIGNATURES: dict[str, tuple] = {
     "kvf_decode_schedule": (
         _i32,
         [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _vp, _i32, _vp,
-         _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
+         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     ),
     "kvf_paged_decode_sched": (
         _i32,
         [_vp, _i32, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp,
-         _i64, _i64, _vp, _i32, _f64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
+         _i64, _i64, _vp, _i32, _f64, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _i64,
+         _vp],
     ),
 }
 

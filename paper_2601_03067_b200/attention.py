@@ -116,6 +116,13 @@ class DecodeSchedule:
     vs: torch.Tensor
     n_items: torch.Tensor
     seq_blocks: torch.Tensor | None = None
+    repeats: int = 0  # slots repeating the previous slot's block inside an item
+
+    @property
+    def dedup(self) -> bool:
+        """Use the run-dedup decode variant: worth its extra bookkeeping once
+        repeats are a visible share of the slots (CFF: ~40%; BFF: ~0)."""
+        return self.repeats * 32 >= self.B * self.p_blocks
 
 
 def decode_schedule(table: torch.Tensor, k_scale: torch.Tensor, v_scale: torch.Tensor,
@@ -136,12 +143,16 @@ def decode_schedule(table: torch.Tensor, k_scale: torch.Tensor, v_scale: torch.T
     ks = torch.empty((nh, cap, ib), dtype=torch.float32, device=dev)
     vs = torch.empty((nh, cap, ib), dtype=torch.float32, device=dev)
     n_items = torch.empty(nh, dtype=torch.int32, device=dev)
+    n_rep = torch.empty(1, dtype=torch.int32, device=dev)
     ws_ints = int(N.lib().kvf_decode_schedule_ws_ints(geom.head_mode, geom.h, geom.NB, B, p_blocks, ib))
     ws = torch.empty(max(ws_ints, 1), dtype=torch.int32, device=dev)
     N.call("kvf_decode_schedule", N.ptr(table), N.ptr(k_scale), N.ptr(v_scale), *geom.args(), layer,
            B, p_blocks, N.ptr(seq_blocks), ib, N.ptr(order), N.ptr(meta), N.ptr(phys), N.ptr(ks),
-           N.ptr(vs), N.ptr(n_items), N.ptr(ws), ws.numel(), N.stream_ptr(stream))
-    return DecodeSchedule(layer, B, p_blocks, ib, order, meta, phys, ks, vs, n_items, seq_blocks)
+           N.ptr(vs), N.ptr(n_items), N.ptr(n_rep), N.ptr(ws), ws.numel(), N.stream_ptr(stream))
+    # one small read per schedule build (once per table change) picks the
+    # decode variant: runs of repeated blocks are decoded once when present
+    return DecodeSchedule(layer, B, p_blocks, ib, order, meta, phys, ks, vs, n_items, seq_blocks,
+                          int(n_rep.item()))
 
 
 def state_decode_schedule(state: FusionState, layer: int, B: int, p_blocks: int, *,
@@ -172,7 +183,7 @@ def _decode_sched(q: torch.Tensor, pool_k, pool_v, geom: Geometry, layer: int, t
         *geom.args(), layer, N.ptr(table), N.ptr(k_scale), N.ptr(v_scale), B, p_blocks,
         N.ptr(sched.seq_blocks), Hq, float(sm_scale), N.ptr(out), N.ptr(lse), sched.item_blocks,
         N.ptr(sched.meta), N.ptr(sched.phys), N.ptr(sched.ks), N.ptr(sched.vs), N.ptr(sched.n_items),
-        N.ptr(workspace), workspace.numel(), N.stream_ptr(stream),
+        1 if sched.dedup else 0, N.ptr(workspace), workspace.numel(), N.stream_ptr(stream),
     )
     return out, lse
 

@@ -62,7 +62,7 @@ __device__ __forceinline__ void load_q_frags(uint32_t (&qa)[D / 16][2], const vo
 }
 }  // namespace
 
-template <int D, int T, int BPT, int DW, int DNS, int IB>
+template <int D, int T, int DW, int DNS, int IB, bool DEDUP>
 __global__ void __launch_bounds__(DW * 32)
 decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap vmap,
                     const void* __restrict__ q, int q_dtype, Geom g, int64_t layer, int64_t B,
@@ -72,15 +72,15 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
                     int64_t cap, float* __restrict__ part) {
   static_assert(2 * IB <= 32, "slot metadata of two items must fit in one warp");
   static_assert(T == 16 || T == 32, "blocks of 16 or 32 tokens");
-  static_assert(IB % BPT == 0 && IB / BPT >= DNS - 1, "the copy lookahead may not pass the next item");
+  static_assert(IB >= DNS - 1, "the copy lookahead may not pass the next item");
   constexpr int HALVES = D / 64;
   constexpr int KS = D / 16;   // k-steps of S^T = K Q^T (head dim)
-  constexpr int MT = BPT * T / 16;  // token m-tiles of S^T = k-steps of O^T = V^T P^T
-  constexpr int TPI = IB / BPT;     // warp tiles per item
+  constexpr int MT = T / 16;   // token m-tiles of S^T = k-steps of O^T = V^T P^T
   constexpr int DT = D / 16;   // head-dim m-tiles of O^T
   constexpr int BOX = T * 128;                 // one (block, d half) box
-  constexpr int TENS = BPT * HALVES * BOX;     // the tile's K (or V) head slices
+  constexpr int TENS = HALVES * BOX;           // one block's K (or V) head slice
   constexpr int STAGE = 2 * TENS;
+  constexpr uint32_t IBMASK = IB == 32 ? 0xffffffffu : ((1u << IB) - 1u);
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* dsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~(uintptr_t)1023);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -114,6 +114,18 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
     ks_l = __ldg(sks + e) * sm_scale;
     vs_l = __ldg(svs + e);
   };
+  // repeats inside an item: bit j set when slot j maps to the same physical
+  // block as slot j - 1 (a request's slots are sorted by physical block, so a
+  // block the request references several times forms one run). A run is
+  // loaded once, its S = K q^T computed once and reused with each slot's
+  // scale, and its P V done once on the scale-weighted sum of the slots' P
+  // (computation reuse of shared blocks).
+  auto dup_mask = [&](int par) -> uint32_t {
+    if constexpr (!DEDUP) return 0u;
+    const int32_t prev = __shfl_up_sync(0xffffffffu, phys_l, 1);
+    const bool d = lane > par * IB && lane < par * IB + IB && phys_l >= 0 && prev == phys_l;
+    return (__ballot_sync(0xffffffffu, d) >> (par * IB)) & IBMASK;
+  };
 
   if (lane == 0) {
     for (int s = 0; s < DNS; ++s) mbar_init(&bars[s], 1);
@@ -129,43 +141,47 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
   load_q_frags<D>(qa, q, q_dtype, meta_cur / nit, kvh_cur, G, Hq, grp, tig);
   __syncwarp();
 
-  // copy issue: tile (item n, block j) into stage s; counters instead of divisions
+  // copy issue: the next run head (item is_n, slot is_j) into stage is_stage
   int is_stage = 0, is_j = 0, is_par = 0;
   int64_t is_n = 0, cur_n = 0;
-  auto issue_next = [&]() {  // all lanes (shuffle); lane 0 issues the copies
+  uint32_t is_dmask = dup_mask(0);
+  auto issue_next = [&]() {  // all lanes (shuffles, ballots); lane 0 issues the copies
+    while (DEDUP && is_n < my_items && ((is_dmask >> is_j) & 1u)) {  // repeats load nothing
+      if (++is_j == IB) {
+        is_j = 0;
+        is_par ^= 1;
+        ++is_n;
+        is_dmask = dup_mask(is_par);
+      }
+    }
     if (is_n >= my_items) return;
-    int32_t ph[BPT];
-#pragma unroll
-    for (int bb = 0; bb < BPT; ++bb)
-      ph[bb] = __shfl_sync(0xffffffffu, phys_l, is_par * IB + is_j * BPT + bb);
+    const int32_t ph = __shfl_sync(0xffffffffu, phys_l, is_par * IB + is_j);
     if (lane == 0) {
       const int kvh = is_n == cur_n ? kvh_cur : kvh_nxt;  // issue runs at most one item ahead
       uint8_t* st = wst + (size_t)is_stage * STAGE;
+      const int row = rowbase + (ph < 0 ? 0 : ph);  // padding loads block 0 (p = 0)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bars[is_stage], (uint32_t)STAGE);
 #pragma unroll
-      for (int bb = 0; bb < BPT; ++bb) {
-        const int row = rowbase + (ph[bb] < 0 ? 0 : ph[bb]);  // padding loads block 0 (p = 0)
-#pragma unroll
-        for (int hf = 0; hf < HALVES; ++hf) {
-          tma4(st + (bb * HALVES + hf) * BOX, &kmap, &bars[is_stage], hf * 64, kvh, 0, row);
-          tma4(st + TENS + (bb * HALVES + hf) * BOX, &vmap, &bars[is_stage], hf * 64, kvh, 0, row);
-        }
+      for (int hf = 0; hf < HALVES; ++hf) {
+        tma4(st + hf * BOX, &kmap, &bars[is_stage], hf * 64, kvh, 0, row);
+        tma4(st + TENS + hf * BOX, &vmap, &bars[is_stage], hf * 64, kvh, 0, row);
       }
     }
     if (++is_stage == DNS) is_stage = 0;
-    if (++is_j == TPI) {
+    if (++is_j == IB) {
       is_j = 0;
       is_par ^= 1;
       ++is_n;
+      if (is_n < my_items) is_dmask = dup_mask(is_par);
     }
   };
   for (int i = 0; i < DNS - 1; ++i) issue_next();
   const int lr = lane & 7, lm = lane >> 3;
-  // swizzled smem address of (token, element) inside the tile's head slices
+  // swizzled smem address of (token, element) inside a block's head slice
   auto addr = [&](uint32_t base, int tok, int e) {
-    const int hf = e >> 6, ch = (e & 63) >> 3, bb = tok / T, tr = tok % T;
-    return base + (uint32_t)((bb * HALVES + hf) * BOX + tr * 128 + ((ch ^ (tr & 7)) << 4));
+    const int hf = e >> 6, ch = (e & 63) >> 3;
+    return base + (uint32_t)(hf * BOX + tok * 128 + ((ch ^ (tok & 7)) << 4));
   };
   int cs_stage = 0;
   uint32_t cs_phase = 0;
@@ -177,6 +193,7 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
     const int64_t b = meta_cur / nit, k = meta_cur % nit;
     const int kvh = kvh_cur;
     cur_n = n;
+    const uint32_t dmask = dup_mask(par);
     if (n > 0) load_info(par ^ 1, gi + NW);  // item n+1 replaces item n-1 (consumed)
     int32_t meta_nn = 0;
     int kvh_nn = 0;
@@ -191,20 +208,18 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
 #pragma unroll
       for (int c = 0; c < 4; ++c) o[mt][c] = 0.f;
 
+    bool q_next_loaded = false;
 #pragma unroll 1
-    for (int j = 0; j < TPI; ++j) {
+    for (int j = 0; j < IB;) {
+      int len = 1;  // run of slots on the same physical block
+      if constexpr (DEDUP)
+        while (j + len < IB && ((dmask >> (j + len)) & 1u)) ++len;
       issue_next();
-      if (j == 1 && has_next)  // next item's query rows, consumed after this item
+      if (!q_next_loaded && has_next) {  // next item's query rows, consumed after this item
         load_q_frags<D>(qn, q, q_dtype, meta_nxt / nit, kvh_nxt, G, Hq, grp, tig);
-      bool valid[BPT];  // padding slot: contributes nothing
-      float ksv[BPT], vsv[BPT];
-#pragma unroll
-      for (int bb = 0; bb < BPT; ++bb) {
-        const int src = par * IB + j * BPT + bb;
-        valid[bb] = __shfl_sync(0xffffffffu, phys_l, src) >= 0;
-        ksv[bb] = __shfl_sync(0xffffffffu, ks_l, src);
-        vsv[bb] = __shfl_sync(0xffffffffu, vs_l, src);
+        q_next_loaded = true;
       }
+      const bool valid = __shfl_sync(0xffffffffu, phys_l, par * IB + j) >= 0;
       mbar_wait(&bars[cs_stage], cs_phase);
       const uint32_t kb = su32(wst + (size_t)cs_stage * STAGE);
       const uint32_t vb = kb + TENS;
@@ -212,7 +227,7 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
         cs_stage = 0;
         cs_phase ^= 1u;
       }
-      // ---- S^T[token][head] = K Q^T: tokens on M, query heads on N ----
+      // ---- S^T[token][head] = K Q^T once per run: tokens on M, query heads on N ----
       float sa[MT][4], sb[MT][4];  // even / odd k-steps (shorter mma chains)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
@@ -230,17 +245,19 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
             mma16816_full(sa[mt], a0, a1, a2, a3, qa[ks][0], qa[ks][1]);
         }
       }
-      // ---- online softmax per head (column); tokens spread over lanes (grp) ----
-      float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int bb = mt * 16 / T;
-          const float lg = valid[bb] ? (sa[mt][c] + sb[mt][c]) * ksv[bb] : -INFINITY;
-          sa[mt][c] = lg;
-          mx[c & 1] = fmaxf(mx[c & 1], lg);
-        }
+        for (int c = 0; c < 4; ++c) sa[mt][c] += sb[mt][c];
+      // ---- online softmax over the run's slots (logits = slot scale x S) ----
+      float mx[2] = {-INFINITY, -INFINITY};
+      for (int r = 0; r < len; ++r) {
+        const float ksr = __shfl_sync(0xffffffffu, ks_l, par * IB + j + r);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) mx[c & 1] = fmaxf(mx[c & 1], valid ? sa[mt][c] * ksr : -INFINITY);
+      }
       float alpha[2];
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
@@ -252,19 +269,23 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
         m_run[hh] = m_new;
         l_run[hh] *= alpha[hh];
       }
-      uint32_t pb[MT][2];  // P^T * v_scale as bf16 pairs (token rows grp / grp + 8)
+      float pe[MT][4];  // sum over the run of P^T * v_scale
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        float pr[4];
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float m = m_run[c & 1];
-          pr[c] = m == -INFINITY ? 0.f : __expf(sa[mt][c] - m);
-          l_run[c & 1] += pr[c];
-        }
-        const float vv = vsv[mt * 16 / T];
-        pb[mt][0] = pack_bf16(pr[0] * vv, pr[1] * vv);
-        pb[mt][1] = pack_bf16(pr[2] * vv, pr[3] * vv);
+        for (int c = 0; c < 4; ++c) pe[mt][c] = 0.f;
+      for (int r = 0; r < len; ++r) {
+        const float ksr = __shfl_sync(0xffffffffu, ks_l, par * IB + j + r);
+        const float vsr = __shfl_sync(0xffffffffu, vs_l, par * IB + j + r);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const float m = m_run[c & 1];
+            const float pr = (!valid || m == -INFINITY) ? 0.f : __expf(sa[mt][c] * ksr - m);
+            l_run[c & 1] += pr;
+            pe[mt][c] = fmaf(pr, vsr, pe[mt][c]);
+          }
       }
 #pragma unroll
       for (int mt = 0; mt < DT; ++mt) {
@@ -277,8 +298,8 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
 #pragma unroll
       for (int kk = 0; kk < MT; ++kk) {
         // B fragment = P^T[token][head]: transpose the two 8x8 token halves
-        const uint32_t b0 = movm_t(pb[kk][0]);
-        const uint32_t b1 = movm_t(pb[kk][1]);
+        const uint32_t b0 = movm_t(pack_bf16(pe[kk][0], pe[kk][1]));
+        const uint32_t b1 = movm_t(pack_bf16(pe[kk][2], pe[kk][3]));
 #pragma unroll
         for (int mt = 0; mt < DT; ++mt) {
           uint32_t a0, a1, a2, a3;
@@ -287,6 +308,7 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
         }
       }
       __syncwarp();  // the stage is refilled by a later issue
+      j += len;
     }
     // ---- item partial (one per request x query head x item) ----
 #pragma unroll
@@ -409,7 +431,7 @@ __global__ void sched_scatter_kernel(const int32_t* __restrict__ item_key,
                                      int64_t B, int64_t p_blocks, int ib,
                                      int32_t* __restrict__ hist, int32_t* __restrict__ meta,
                                      int32_t* __restrict__ sphys, float* __restrict__ sks,
-                                     float* __restrict__ svs) {
+                                     float* __restrict__ svs, int32_t* __restrict__ n_repeats) {
   const int64_t hu = blockIdx.y;
   const int64_t unit = g.head_mode ? layer * g.h + hu : layer;
   const int64_t nit = (p_blocks + ib - 1) / ib;
@@ -422,6 +444,7 @@ __global__ void sched_scatter_kernel(const int32_t* __restrict__ item_key,
     meta[pos] = (int32_t)x;
     const int64_t b = x / nit, k = x % nit;
     const int32_t* ord = order + (hu * B + b) * p_blocks;
+    int32_t prev = -1, reps = 0;
     for (int j = 0; j < ib; ++j) {
       const int64_t jj = k * ib + j;
       const int32_t o = jj < p_blocks ? ord[jj] : -1;
@@ -436,7 +459,10 @@ __global__ void sched_scatter_kernel(const int32_t* __restrict__ item_key,
       sphys[pos * ib + j] = ph;
       sks[pos * ib + j] = ksv;
       svs[pos * ib + j] = vsv;
+      if (j > 0 && ph >= 0 && ph == prev) ++reps;
+      prev = ph;
     }
+    if (reps && n_repeats) atomicAdd(n_repeats, reps);
   }
 }
 
@@ -468,13 +494,15 @@ cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, c
                                    const Geom& g, int64_t layer, int64_t B, int64_t p_blocks,
                                    const int32_t* seq_blocks, int ib, int32_t* order,
                                    int32_t* meta, int32_t* phys, float* ks, float* vs,
-                                   int32_t* n_items, int32_t* ws, cudaStream_t s) {
+                                   int32_t* n_items, int32_t* n_repeats, int32_t* ws,
+                                   cudaStream_t s) {
   const int64_t nh = g.head_mode ? g.h : 1;
   const int64_t nit = (p_blocks + ib - 1) / ib;
   int32_t* hist = ws;
   int32_t* item_key = ws + nh * g.NB;
   cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * nh * g.NB, s);
   if (e != cudaSuccess) return e;
+  if (n_repeats && (e = cudaMemsetAsync(n_repeats, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
   if (B == 0) return cudaMemsetAsync(n_items, 0, sizeof(int32_t) * nh, s);
   int sortn = 1;
   while (sortn < p_blocks) sortn <<= 1;
@@ -491,18 +519,19 @@ cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, c
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const int64_t n = B * nit;
   sched_scatter_kernel<<<dim3((unsigned)std::min<int64_t>((n + 127) / 128, 8192), (unsigned)nh), 128, 0, s>>>(
-      item_key, order, table, k_scale, v_scale, g, layer, B, p_blocks, ib, hist, meta, phys, ks, vs);
+      item_key, order, table, k_scale, v_scale, g, layer, B, p_blocks, ib, hist, meta, phys, ks, vs,
+      n_repeats);
   return cudaGetLastError();
 }
 
 namespace {
-template <int D, int T, int BPT, int DW, int DNS, int IB>
+template <int D, int T, int DW, int DNS, int IB, bool DEDUP>
 cudaError_t decode_sched_t(const DecodeArgs& a, cudaStream_t s) {
   CUtensorMap km, vm;
   if (!make_map(&km, a.pool_k, a.g) || !make_map(&vm, a.pool_v, a.g)) return cudaErrorInvalidValue;
-  constexpr int STAGE = 2 * BPT * (D / 64) * T * 128;
+  constexpr int STAGE = 2 * (D / 64) * T * 128;
   constexpr int smem = 1024 + DW * DNS * STAGE + DW * DNS * 8;
-  auto kern = decode_sched_kernel<D, T, BPT, DW, DNS, IB>;
+  auto kern = decode_sched_kernel<D, T, DW, DNS, IB, DEDUP>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -540,8 +569,15 @@ cudaError_t decode_sched_ib(const DecodeArgs& a, cudaStream_t s) {
   // per tile: 6 x 2 141.0, 4 x 3 164.4 (the warp loop is latency bound: warps per
   // SM -- balanced over the 4 schedulers -- beat deeper rings and larger tiles).
   constexpr int DW = T == 16 ? 12 : 6;
-  if (a.sched->ib == 16) return decode_sched_t<D, T, 1, DW, 2, 16>(a, s);
-  if (a.sched->ib == 8) return decode_sched_t<D, T, 1, DW, 2, 8>(a, s);
+  // runs of repeated blocks (CFF, in-request sharing) take the dedup variant;
+  // caches without repeats keep the leaner loop
+  if (a.sched->dedup) {
+    if (a.sched->ib == 16) return decode_sched_t<D, T, DW, 2, 16, true>(a, s);
+    if (a.sched->ib == 8) return decode_sched_t<D, T, DW, 2, 8, true>(a, s);
+  } else {
+    if (a.sched->ib == 16) return decode_sched_t<D, T, DW, 2, 16, false>(a, s);
+    if (a.sched->ib == 8) return decode_sched_t<D, T, DW, 2, 8, false>(a, s);
+  }
   return cudaErrorInvalidValue;
 }
 }  // namespace

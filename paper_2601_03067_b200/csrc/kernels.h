@@ -170,6 +170,7 @@ struct SchedView {
   const int32_t* n_items;
   int64_t cap;
   int ib;
+  int dedup;  // runs of repeated blocks inside items (decode them once)
 };
 bool decode_sched_item_blocks_ok(int ib);
 bool decode_sched_shape_ok(int t, int d);  // one block per warp tile: t in {16, 32}
@@ -178,7 +179,8 @@ cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, c
                                    const Geom& g, int64_t layer, int64_t B, int64_t p_blocks,
                                    const int32_t* seq_blocks, int ib, int32_t* order,
                                    int32_t* meta, int32_t* phys, float* ks, float* vs,
-                                   int32_t* n_items, int32_t* ws, cudaStream_t s);
+                                   int32_t* n_items, int32_t* n_repeats, int32_t* ws,
+                                   cudaStream_t s);
 cudaError_t launch_decode_sched(const DecodeArgs& a, cudaStream_t s);
 // out[i] = map[ids[i]] for 0 <= ids[i] < map_len, else -1 (compaction: slot
 // tables / schedule ids -> dense rows of a compacted pool)

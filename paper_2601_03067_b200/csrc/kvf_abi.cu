@@ -398,8 +398,8 @@ int kvf_decode_schedule(const int32_t* table, const void* k_scale, const void* v
                         int64_t NB, int t, int h, int d, int head_mode, int64_t layer, int64_t B,
                         int64_t p_blocks, const int32_t* seq_blocks, int item_blocks,
                         int32_t* order, int32_t* meta, int32_t* phys, float* ks, float* vs,
-                        int32_t* n_items, int32_t* workspace, int64_t workspace_ints,
-                        void* stream) {
+                        int32_t* n_items, int32_t* n_repeats, int32_t* workspace,
+                        int64_t workspace_ints, void* stream) {
   Geom g;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
   if (layer < 0 || layer >= L) return fail(KVF_ERR_INVALID, "layer out of range");
@@ -416,7 +416,7 @@ int kvf_decode_schedule(const int32_t* table, const void* k_scale, const void* v
     return fail(KVF_ERR_INVALID, "schedule workspace too small");
   return cuda_status(launch_decode_schedule(table, (const float*)k_scale, (const float*)v_scale, g,
                                             layer, B, p_blocks, seq_blocks, item_blocks, order,
-                                            meta, phys, ks, vs, n_items, workspace,
+                                            meta, phys, ks, vs, n_items, n_repeats, workspace,
                                             (cudaStream_t)stream),
                      "kvf_decode_schedule");
 }
@@ -427,10 +427,10 @@ int kvf_paged_decode_sched(const void* q, int q_dtype, const void* pool_k, const
                            const void* v_scale, int64_t B, int64_t p_blocks,
                            const int32_t* seq_blocks, int Hq, double sm_scale, void* out,
                            void* lse, int item_blocks, const int32_t* meta, const int32_t* phys,
-                           const float* ks, const float* vs, const int32_t* n_items,
+                           const float* ks, const float* vs, const int32_t* n_items, int dedup,
                            void* workspace, int64_t workspace_bytes, void* stream) {
   const int64_t nit = item_blocks > 0 ? (p_blocks + item_blocks - 1) / item_blocks : 0;
-  SchedView v{meta, phys, ks, vs, n_items, B * nit, item_blocks};
+  SchedView v{meta, phys, ks, vs, n_items, B * nit, item_blocks, dedup ? 1 : 0};
   if (workspace_bytes < B * Hq * nit * (int64_t)(d + 2) * 4)
     return fail(KVF_ERR_INVALID, "decode workspace too small");
   return paged_decode_impl(q, q_dtype, pool_k, pool_v, dtype, L, NB, t, h, d, head_mode, layer,

@@ -65,16 +65,16 @@ def test_schedule_and_compaction_argument_errors():
     assert lib.kvf_decode_schedule_ws_ints(0, 8, 1024, 4, 256, 5) < 0  # bad item size
     # B * p_blocks beyond the layer's slots
     rc = lib.kvf_decode_schedule(None, None, None, 1, 100, 16, 8, 128, 0, 0, 4, 32, None, 16,
-                                 None, None, None, None, None, None, None, 0, None)
+                                 None, None, None, None, None, None, None, None, 0, None)
     assert rc == N.KVF_ERR_INVALID and "exceeds" in lib.kvf_last_error().decode()
     # unsupported item size
     rc = lib.kvf_decode_schedule(None, None, None, 1, 1024, 16, 8, 128, 0, 0, 4, 32, None, 12,
-                                 None, None, None, None, None, None, None, 0, None)
+                                 None, None, None, None, None, None, None, None, 0, None)
     assert rc == N.KVF_ERR_INVALID and "item_blocks" in lib.kvf_last_error().decode()
     # scheduled decode: probabilities are not offered, GQA group limit
     rc = lib.kvf_paged_decode_sched(None, 2, None, None, 2, 1, 1024, 16, 8, 128, 0, 0, None, None,
                                     None, 4, 32, None, 80, 0.1, None, None, 16, None, None, None,
-                                    None, None, None, 1 << 20, None)
+                                    None, None, 0, None, 1 << 20, None)
     assert rc == N.KVF_ERR_INVALID
     assert lib.kvf_remap_ids(None, -1, None, 0, None, None) == N.KVF_ERR_INVALID
     assert lib.kvf_remap_ids(None, 0, None, 0, None, None) == N.KVF_OK  # empty: nothing to do

@@ -151,3 +151,27 @@ def test_scheduled_decode_many_sharers():
     got, _ = K.paged_decode(q, st, 0, B, p, schedule=sched)
     want = _reference(q, st, 0, B, p)
     torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
+
+
+@pytest.mark.parametrize("ib", [8, 16])
+def test_scheduled_decode_cff_repeats(ib):
+    """CFF shares blocks inside a request: a request's context holds the same
+    fused block several times (runs in the sorted slot order). Runs are loaded
+    and multiplied once; the result must equal the slot-by-slot reference."""
+    L, B, p, t, h, d = 1, 6, 64, 16, 4, 128
+    Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=53, variant="cff")
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    outs = K.fuse_chunks(cache, K.FusionConfig(threshold=0.8, variant="cff"), 4 * t, keep_samples=False)
+    st = outs[0].fused.state
+    tab = st.table[0].view(B, p)
+    repeats = sum(int(len(r) - len(torch.unique(r))) for r in tab)
+    assert repeats > B * p // 4  # CFF: many in-request repeats
+    q = torch.randn((B, 4 * h, d), device="cuda", dtype=torch.bfloat16)
+    seq = torch.tensor([p, 63, 1, 40, 17, p], dtype=torch.int32, device="cuda")
+    for sb in (None, seq):
+        sched = K.state_decode_schedule(st, 0, B, p, seq_blocks=sb, item_blocks=ib)
+        got, lse = K.paged_decode(q, st, 0, B, p, schedule=sched)
+        want = _reference(q, st, 0, B, p, sb)
+        torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
+        plain, lse0 = K.paged_decode(q, st, 0, B, p, seq_blocks=sb)
+        torch.testing.assert_close(lse, lse0, atol=1e-3, rtol=1e-3)

@@ -52,6 +52,7 @@ o1, _ = K.paged_decode(q, st, 0, B, p)
 o2, _ = K.paged_decode(q, st, 0, B, p, schedule=scheds[0])
 err = (o1 - o2).abs().max().item()
 tsch = timeit(lambda: [K.state_decode_schedule(st, l, B, p, item_blocks=IB) for l in range(L)], n=3)
+print(f"repeats/layer={scheds[0].repeats} dedup={scheds[0].dedup}")
 print(f"IB={IB} L={L} B={B} ctx={p * t} CR={cr:.3f} logical MB/layer={logical / 1e6:.0f} unique MB/layer={logical / cr / 1e6:.0f}")
 for k, v in res.items():
     print(f"  {k:12s} {v * 1e3:8.1f} us/layer  logical {logical / v / 1e6:7.0f} GB/s  tok/s(32 layers) {B / (v * 32 / 1e3):9.0f}")
