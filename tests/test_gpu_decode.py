@@ -175,3 +175,19 @@ def test_scheduled_decode_cff_repeats(ib):
         torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
         plain, lse0 = K.paged_decode(q, st, 0, B, p, seq_blocks=sb)
         torch.testing.assert_close(lse, lse0, atol=1e-3, rtol=1e-3)
+
+
+@pytest.mark.parametrize("t,d", [(32, 128), (32, 64), (16, 64)])
+def test_scheduled_decode_block_sizes(t, d):
+    """32-token blocks (6-warp variant) and d = 64 through the scheduled path."""
+    L, B, p, h = 1, 5, 24, 2
+    Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=71)
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    st = K.fuse_batch(cache, K.FusionConfig(threshold=0.8), keep_samples=False)[0].fused.state
+    q = torch.randn((B, 3 * h, d), device="cuda", dtype=torch.bfloat16)
+    seq = torch.tensor([p, 3, 24, 11, 1], dtype=torch.int32, device="cuda")
+    for sb in (None, seq):
+        sched = K.state_decode_schedule(st, 0, B, p, seq_blocks=sb)
+        got, _ = K.paged_decode(q, st, 0, B, p, schedule=sched)
+        want = _reference(q, st, 0, B, p, sb)
+        torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
