@@ -316,7 +316,7 @@ def ours_main(args):
     from paper_2601_03067_b200 import CacheDims, FusionConfig, PagedKvCache, fuse_batch, fuse_chunks
     from paper_2601_03067_b200 import _native as N
     from paper_2601_03067_b200.core import cff_layout
-    from paper_2601_03067_b200.engine import FusionEngine, Geometry
+    from paper_2601_03067_b200.engine import RESCORE_BAND, FusionEngine, Geometry
     from paper_2601_03067_b200.schedule import bff_plan, cff_plan
     from paper_2601_03067_b200.workload import synthetic_kv
 
@@ -441,6 +441,15 @@ def ours_main(args):
                           + ("; each step one CUDA-graph replay" if graph is not None else ""),
             },
             "compression_ratio": cr,
+            "parity": {
+                "near_threshold_pairs_per_step": int(sum(int(x.item()) for x in st_last.near_threshold)),
+                "rescore_band": RESCORE_BAND if engine.path == N.PATH_TC else 0.0,
+                "note": "similarity pairs within rescore_band of the threshold are re-decided in "
+                        "float64 from the stored blocks (level 1: exact reference decisions); "
+                        "tests/test_gpu_fullsize.py checks level-1 decisions and similarity-sum "
+                        "linearity at this size, tests/test_gpu_parity.py the whole tree vs the "
+                        "float64 oracle (bf16 eps 1e-3 for levels >= 2, flips counted)",
+            },
             "sim_path": {N.PATH_TC: "tcgen05", N.PATH_SIMT: "simt"}[engine.path],
             "roofline": {
                 "kernel": "sim_tc_kernel (K2+K3 similarity GEMM + first-match epilogue)",

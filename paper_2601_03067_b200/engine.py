@@ -152,6 +152,7 @@ class FusionState:
     level_samples: list[torch.Tensor | None] = field(default_factory=list)
     launches: int = 0
     sim_events: list = field(default_factory=list)  # (start, end, level) CUDA events
+    near_threshold: list = field(default_factory=list)  # per level int32[1]: re-scored pairs
 
 
 class FusionEngine:
@@ -296,6 +297,8 @@ class FusionEngine:
             )
             if self.rescore_cap:
                 launches += 1
+                # pairs within RESCORE_BAND of the threshold at this level (decided in float64)
+                st.near_threshold.append(self.rescore[4 * self.rescore_cap:4 * self.rescore_cap + 1].clone())
             if time_sim:
                 e1.record(stream)
                 st.sim_events.append((e0, e1, li))
