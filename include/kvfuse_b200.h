@@ -208,6 +208,23 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
                      void* out, void* lse, void* probs, void* workspace,
                      int64_t workspace_bytes, void* stream);
 
+/* Chunked-prefill attention over a CFF-fused context with computation reuse
+ * (PAPER.md:57-59, 130-131): the queries of chunk `chunk`
+ * (bf16 [B][chunk_blocks*t][Hq][d]) attend to the logical keys of chunks
+ * 0..chunk-1 (all visible) and causally to the chunk's own keys, every slot
+ * read through table / k_scale / v_scale (core.py:303-304). order: int32
+ * [B][p_blocks] each request's positions sorted by physical block (the decode
+ * schedule's `order`). dedup = 1: S = Q K_P^T and P V_P once per physical
+ * block P with the slots' scales folded in; dedup = 0: once per slot.
+ * out: float32 [B][chunk_blocks*t][Hq][d]. bf16, folded, t = 16, Hq/h | 8. */
+int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v,
+                      int dtype, int64_t L, int64_t NB, int t, int h, int d,
+                      int head_mode, int64_t layer, const int32_t* table,
+                      const void* k_scale, const void* v_scale,
+                      const int32_t* order, int64_t B, int64_t p_blocks,
+                      int chunk_blocks, int chunk, int Hq, double sm_scale,
+                      int dedup, void* out, void* stream);
+
 /* Percentile mode of the threshold controller on the device (fusion.py:418-437,
  * SURVEY §8f rank 3): *out = np.quantile(x, q) (numpy's default 'linear'
  * method) over the non-NaN entries of nparts float64 device segments

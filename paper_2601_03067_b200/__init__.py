@@ -10,6 +10,7 @@ from .attention import (
     SoftmaxDistribution,
     DecodeSchedule,
     attention_drift,
+    chunk_prefill,
     decode_schedule,
     state_decode_schedule,
     paged_attention,
@@ -67,7 +68,7 @@ __all__ = [
     "FusedCache", "FusedLayer", "FusionConfig", "FusionEngine", "FusionEvent", "FusionOutcome",
     "FusionReport", "FusionState", "Geometry", "InsufficientDataError", "InvalidCacheError",
     "KvFuseError", "LayerView", "MergeRecord", "PagedKvCache", "SoftmaxDistribution",
-    "UnfoldedLayer", "ZeroVectorError", "adapt_threshold", "attention_drift", "cff_chunk_count",
+    "UnfoldedLayer", "ZeroVectorError", "adapt_threshold", "attention_drift", "cff_chunk_count", "chunk_prefill",
     "DecodeSchedule", "cosine_similarity", "decode_schedule", "fast_fusion", "fuse_batch", "fuse_chunks", "paged_attention",
     "paged_decode", "refold", "reports_to_csv", "softmax", "state_decode_schedule", "tune_threshold", "unfold_bff",
     "unfold_cff",

@@ -83,6 +83,11 @@ SIGNATURES: dict[str, tuple] = {
          _i64, _i64, _vp, _i32, _f64, _vp, _vp, _vp, _vp, _i64, _vp],
     ),
     "kvf_remap_ids": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp]),
+    "kvf_chunk_prefill": (
+        _i32,
+        [_vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _i64,
+         _i64, _i32, _i32, _i32, _f64, _i32, _vp, _vp],
+    ),
     "kvf_quantile_ws_bytes": (_i64, []),
     "kvf_quantile": (_i32, [_vp, _vp, _i32, _f64, _vp, _vp, _i64, _vp]),
     "kvf_decode_schedule_item_blocks": (_i32, []),

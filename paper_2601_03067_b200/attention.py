@@ -188,6 +188,33 @@ def _decode_sched(q: torch.Tensor, pool_k, pool_v, geom: Geometry, layer: int, t
     return out, lse
 
 
+def chunk_prefill(q: torch.Tensor, state: FusionState, layer: int, B: int, p_blocks: int,
+                  chunk_blocks: int, chunk: int, *, order: torch.Tensor | None = None,
+                  dedup: bool = True, sm_scale: float | None = None, out=None,
+                  stream=None) -> torch.Tensor:
+    """Chunked-prefill attention of chunk `chunk` over a CFF-fused layer
+    (kvf_chunk_prefill): q bf16 [B, chunk_blocks*t, Hq, d]
+    attends to the keys of the earlier chunks and, causally, to its own chunk,
+    all read through the fused table and per-slot scales. With `dedup` the
+    Q K^T and P V work runs once per physical block, not once per slot.
+    `order` = each request's positions sorted by physical block (a decode
+    schedule's `order[0]`); built here when omitted. Returns fp32 out."""
+    g = state.geom
+    if order is None:
+        order = state_decode_schedule(state, layer, B, p_blocks).order[0]
+    Hq = q.shape[2]
+    sc = sm_scale if sm_scale is not None else 1.0 / float(np.sqrt(g.d))
+    if out is None:
+        out = torch.empty((B, chunk_blocks * g.t, Hq, g.d), dtype=torch.float32, device=q.device)
+    if q.dtype != torch.bfloat16 or not q.is_contiguous():
+        raise InvalidCacheError("chunk_prefill takes contiguous bf16 queries")
+    N.call("kvf_chunk_prefill", N.ptr(q), N.ptr(state.pool_k), N.ptr(state.pool_v),
+           dtype_code(state.pool_k.dtype), *g.args(), layer, N.ptr(state.table), N.ptr(state.k_scale),
+           N.ptr(state.v_scale), N.ptr(order), B, p_blocks, chunk_blocks, chunk, Hq, float(sc),
+           1 if dedup else 0, N.ptr(out), N.stream_ptr(stream))
+    return out
+
+
 def paged_decode(q: torch.Tensor, state: FusionState, layer: int, B: int, p_blocks: int, *,
                  sm_scale: float | None = None, seq_blocks: torch.Tensor | None = None,
                  schedule: DecodeSchedule | None = None, out=None, lse=None, workspace=None,

@@ -182,6 +182,28 @@ cudaError_t launch_decode_schedule(const int32_t* table, const float* k_scale, c
                                    int32_t* n_items, int32_t* n_repeats, int32_t* ws,
                                    cudaStream_t s);
 cudaError_t launch_decode_sched(const DecodeArgs& a, cudaStream_t s);
+// chunked-prefill attention over a CFF-fused context with computation reuse
+// (kern_prefill.cu): queries of chunk `chunk` of every request against the
+// earlier chunks' keys (all visible) and the chunk's own keys (causal)
+struct ChunkPrefillArgs {
+  const void* q;  // bf16 [B][chunk_blocks * t][Hq][d]
+  const void* pool_k;
+  const void* pool_v;
+  Geom g;
+  int64_t layer;
+  const int32_t* table;
+  const float* k_scale;
+  const float* v_scale;
+  const int32_t* order;  // [B][p_blocks] positions sorted by physical block (-1 = none)
+  int64_t B, p_blocks;
+  int chunk_blocks, chunk, Hq;
+  double sm_scale;
+  int dedup;
+  float* out;  // [B][chunk_blocks * t][Hq][d]
+};
+bool chunk_prefill_supported(const ChunkPrefillArgs& a, const char** why);
+cudaError_t launch_chunk_prefill(const ChunkPrefillArgs& a, cudaStream_t s);
+
 // out[i] = map[ids[i]] for 0 <= ids[i] < map_len, else -1 (compaction: slot
 // tables / schedule ids -> dense rows of a compacted pool)
 cudaError_t launch_remap_ids(const int32_t* ids, int64_t n, const int32_t* map, int64_t map_len,

@@ -386,6 +386,40 @@ int kvf_quantile(const void* const* parts, const int64_t* lens, int nparts, doub
                      "kvf_quantile");
 }
 
+int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v, int dtype, int64_t L,
+                      int64_t NB, int t, int h, int d, int head_mode, int64_t layer,
+                      const int32_t* table, const void* k_scale, const void* v_scale,
+                      const int32_t* order, int64_t B, int64_t p_blocks, int chunk_blocks,
+                      int chunk, int Hq, double sm_scale, int dedup, void* out, void* stream) {
+  ChunkPrefillArgs a;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
+  if (dtype != BF16) return fail(KVF_ERR_INVALID, "chunked prefill needs bf16 pools");
+  if (layer < 0 || layer >= L) return fail(KVF_ERR_INVALID, "layer out of range");
+  if (B < 0 || p_blocks < 1 || B * p_blocks > NB || chunk_blocks < 1 || Hq < 1 || Hq % h)
+    return fail(KVF_ERR_INVALID, "bad batch / chunk / head shape");
+  if (B > 0 && (!q || !pool_k || !pool_v || !table || !k_scale || !v_scale || !order || !out))
+    return fail(KVF_ERR_INVALID, "null pointer");
+  a.q = q;
+  a.pool_k = pool_k;
+  a.pool_v = pool_v;
+  a.layer = layer;
+  a.table = table;
+  a.k_scale = (const float*)k_scale;
+  a.v_scale = (const float*)v_scale;
+  a.order = order;
+  a.B = B;
+  a.p_blocks = p_blocks;
+  a.chunk_blocks = chunk_blocks;
+  a.chunk = chunk;
+  a.Hq = Hq;
+  a.sm_scale = sm_scale;
+  a.dedup = dedup ? 1 : 0;
+  a.out = (float*)out;
+  const char* why = "";
+  if (!chunk_prefill_supported(a, &why)) return fail(KVF_ERR_INVALID, "chunked prefill: %s", why);
+  return cuda_status(launch_chunk_prefill(a, (cudaStream_t)stream), "kvf_chunk_prefill");
+}
+
 int kvf_decode_schedule_item_blocks(void) { return 16; }
 
 int64_t kvf_decode_schedule_ws_ints(int head_mode, int h, int64_t NB, int64_t B, int64_t p_blocks,
