@@ -186,45 +186,57 @@ chunk_prefill_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
 #pragma unroll
     for (int c = 0; c < 4; ++c) o[et][c] = 0.f;
 
-  for (int u = 0; u < nu; ++u) {
-    const int s = u % PF_STAGES;
-    mbar_wait(&full[s], (u / PF_STAGES) & 1);
-    const uint32_t kb = su32(dsm + (size_t)s * STAGE);
-    const uint32_t vb = kb + TENS;
-    // S = Q K^T: 16 query rows x 16 keys (2 n-tiles)
-    float sc[2][4];
+  // units are consumed in groups of UG (UG * 16 keys per online-softmax step):
+  // the QK products of the group are independent (ILP), the max / rescale once
+  constexpr int UG = 4;
+  for (int u0 = 0; u0 < nu; u0 += UG) {
+    const int ng = min(UG, nu - u0);
+    float sc[UG][2][4];
+    uint32_t vmask = 0;  // bit (i * 8 + nn * 4 + c): logit visible (causal)
 #pragma unroll
-    for (int nn = 0; nn < 2; ++nn)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) sc[nn][c] = 0.f;
-#pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      uint32_t r0, r1, r2, r3;
-      ldsm_x4(addr(kb, (lm >> 1) * 8 + lr, ks * 16 + (lm & 1) * 8), r0, r1, r2, r3);
-      mma16816_full(sc[0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], r0, r1);
-      mma16816_full(sc[1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], r2, r3);
-    }
-    const int kbase = u_kbase[u];
-    const int sb = u_beg[u], se = u_beg[u + 1];
-    // causal visibility of this thread's 8 logits (own-chunk units only)
-    bool vis[2][4];
-#pragma unroll
-    for (int nn = 0; nn < 2; ++nn)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int key = kbase + nn * 8 + 2 * tig + (c & 1);
-        const int qi = qi0 + ((c >> 1) ? 8 : 0);
-        vis[nn][c] = kbase < 0 || key <= qi;
-      }
-    // online softmax over the unit's slots (logits = k_scale[s] * S)
-    float mx[2] = {-INFINITY, -INFINITY};
-    for (int r = sb; r < se; ++r) {
-      const float ksr = s_ks[r];
+    for (int i = 0; i < UG; ++i) {
 #pragma unroll
       for (int nn = 0; nn < 2; ++nn)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (vis[nn][c]) mx[c >> 1] = fmaxf(mx[c >> 1], sc[nn][c] * ksr);
+        for (int c = 0; c < 4; ++c) sc[i][nn][c] = 0.f;
+      if (i < ng) {
+        const int u = u0 + i;
+        const int s = u % PF_STAGES;
+        mbar_wait(&full[s], (u / PF_STAGES) & 1);
+        const uint32_t kb = su32(dsm + (size_t)s * STAGE);
+        // S = Q K^T: 16 query rows x 16 keys (2 n-tiles)
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          uint32_t r0, r1, r2, r3;
+          ldsm_x4(addr(kb, (lm >> 1) * 8 + lr, ks * 16 + (lm & 1) * 8), r0, r1, r2, r3);
+          mma16816_full(sc[i][0], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], r0, r1);
+          mma16816_full(sc[i][1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], r2, r3);
+        }
+        const int kbase = u_kbase[u];
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int key = kbase + nn * 8 + 2 * tig + (c & 1);
+            const int qi = qi0 + ((c >> 1) ? 8 : 0);
+            if (kbase < 0 || key <= qi) vmask |= 1u << (i * 8 + nn * 4 + c);
+          }
+      }
+    }
+    // online softmax over the group's slots (logits = k_scale[s] * S)
+    float mx[2] = {-INFINITY, -INFINITY};
+#pragma unroll
+    for (int i = 0; i < UG; ++i) {
+      if (i >= ng) break;
+      const int sb = u_beg[u0 + i], se = u_beg[u0 + i + 1];
+      for (int r = sb; r < se; ++r) {
+        const float ksr = s_ks[r];
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if ((vmask >> (i * 8 + nn * 4 + c)) & 1u) mx[c >> 1] = fmaxf(mx[c >> 1], sc[i][nn][c] * ksr);
+      }
     }
     float alpha[2];
 #pragma unroll
@@ -236,44 +248,55 @@ chunk_prefill_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_cons
       m_run[hr] = m_new;
       l_run[hr] *= alpha[hr];
     }
-    float pe[2][4];
+    if (__any_sync(0xffffffffu, alpha[0] != 1.f || alpha[1] != 1.f)) {
 #pragma unroll
-    for (int nn = 0; nn < 2; ++nn)
+      for (int et = 0; et < NE; ++et) {
+        o[et][0] *= alpha[0];
+        o[et][1] *= alpha[0];
+        o[et][2] *= alpha[1];
+        o[et][3] *= alpha[1];
+      }
+    }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) pe[nn][c] = 0.f;
-    for (int r = sb; r < se; ++r) {
-      const float ksr = s_ks[r], vsr = s_vs[r];
+    for (int i = 0; i < UG; ++i) {
+      if (i >= ng) break;
+      const int u = u0 + i;
+      const int s = u % PF_STAGES;
+      const uint32_t vb = su32(dsm + (size_t)s * STAGE) + TENS;
+      float pe[2][4];
 #pragma unroll
       for (int nn = 0; nn < 2; ++nn)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const float m = m_run[c >> 1];
-          const float pr = (vis[nn][c] && m != -INFINITY) ? __expf(sc[nn][c] * ksr - m) : 0.f;
-          l_run[c >> 1] += pr;
-          pe[nn][c] = fmaf(pr, vsr, pe[nn][c]);
-        }
-    }
+        for (int c = 0; c < 4; ++c) pe[nn][c] = 0.f;
+      const int sb = u_beg[u], se = u_beg[u + 1];
+      for (int r = sb; r < se; ++r) {
+        const float ksr = s_ks[r], vsr = s_vs[r];
 #pragma unroll
-    for (int et = 0; et < NE; ++et) {
-      o[et][0] *= alpha[0];
-      o[et][1] *= alpha[0];
-      o[et][2] *= alpha[1];
-      o[et][3] *= alpha[1];
-    }
-    // O += P_eff V: A = P_eff (C layout of S maps to the A layout), B = V
-    const uint32_t a0 = pack_bf16(pe[0][0], pe[0][1]);
-    const uint32_t a1 = pack_bf16(pe[0][2], pe[0][3]);
-    const uint32_t a2 = pack_bf16(pe[1][0], pe[1][1]);
-    const uint32_t a3 = pack_bf16(pe[1][2], pe[1][3]);
+        for (int nn = 0; nn < 2; ++nn)
 #pragma unroll
-    for (int et = 0; et < NE; et += 2) {
-      uint32_t r0, r1, r2, r3;
-      ldsm_x4_t(addr(vb, (lm & 1) * 8 + lr, et * 8 + (lm >> 1) * 8), r0, r1, r2, r3);
-      mma16816_full(o[et], a0, a1, a2, a3, r0, r1);
-      mma16816_full(o[et + 1], a0, a1, a2, a3, r2, r3);
+          for (int c = 0; c < 4; ++c) {
+            const float m = m_run[c >> 1];
+            const bool v = (vmask >> (i * 8 + nn * 4 + c)) & 1u;
+            const float pr = (v && m != -INFINITY) ? __expf(sc[i][nn][c] * ksr - m) : 0.f;
+            l_run[c >> 1] += pr;
+            pe[nn][c] = fmaf(pr, vsr, pe[nn][c]);
+          }
+      }
+      // O += P_eff V: A = P_eff (C layout of S maps to the A layout), B = V
+      const uint32_t a0 = pack_bf16(pe[0][0], pe[0][1]);
+      const uint32_t a1 = pack_bf16(pe[0][2], pe[0][3]);
+      const uint32_t a2 = pack_bf16(pe[1][0], pe[1][1]);
+      const uint32_t a3 = pack_bf16(pe[1][2], pe[1][3]);
+#pragma unroll
+      for (int et = 0; et < NE; et += 2) {
+        uint32_t r0, r1, r2, r3;
+        ldsm_x4_t(addr(vb, (lm & 1) * 8 + lr, et * 8 + (lm >> 1) * 8), r0, r1, r2, r3);
+        mma16816_full(o[et], a0, a1, a2, a3, r0, r1);
+        mma16816_full(o[et + 1], a0, a1, a2, a3, r2, r3);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_local(&empty[s]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive_local(&empty[s]);
   }
   // ---- normalise and store: out[b][token][qh][d] (fp32) ----
 #pragma unroll
