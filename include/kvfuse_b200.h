@@ -216,14 +216,16 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
  * [B][p_blocks] each request's positions sorted by physical block (the decode
  * schedule's `order`). dedup = 1: S = Q K_P^T and P V_P once per physical
  * block P with the slots' scales folded in; dedup = 0: once per slot.
- * out: float32 [B][chunk_blocks*t][Hq][d]. bf16, folded, t = 16, Hq/h | 8. */
+ * out: float32 [B][chunk_blocks*t][Hq][d]. bf16, folded, t = 16, Hq/h | 8.
+ * path: 0 auto (mma.sync), 1 mma.sync kernel, 2 tcgen05 kernel (d = 128: S
+ * and P V on the tensor cores, accumulators in TMEM, 4 units per softmax step). */
 int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v,
                       int dtype, int64_t L, int64_t NB, int t, int h, int d,
                       int head_mode, int64_t layer, const int32_t* table,
                       const void* k_scale, const void* v_scale,
                       const int32_t* order, int64_t B, int64_t p_blocks,
                       int chunk_blocks, int chunk, int Hq, double sm_scale,
-                      int dedup, void* out, void* stream);
+                      int dedup, int path, void* out, void* stream);
 
 /* Percentile mode of the threshold controller on the device (fusion.py:418-437,
  * SURVEY §8f rank 3): *out = np.quantile(x, q) (numpy's default 'linear'

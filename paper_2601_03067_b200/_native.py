@@ -86,7 +86,7 @@ SIGNATURES: dict[str, tuple] = {
     "kvf_chunk_prefill": (
         _i32,
         [_vp, _vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _i64,
-         _i64, _i32, _i32, _i32, _f64, _i32, _vp, _vp],
+         _i64, _i32, _i32, _i32, _f64, _i32, _i32, _vp, _vp],
     ),
     "kvf_quantile_ws_bytes": (_i64, []),
     "kvf_quantile": (_i32, [_vp, _vp, _i32, _f64, _vp, _vp, _i64, _vp]),

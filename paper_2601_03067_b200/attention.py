@@ -190,8 +190,8 @@ def _decode_sched(q: torch.Tensor, pool_k, pool_v, geom: Geometry, layer: int, t
 
 def chunk_prefill(q: torch.Tensor, state: FusionState, layer: int, B: int, p_blocks: int,
                   chunk_blocks: int, chunk: int, *, order: torch.Tensor | None = None,
-                  dedup: bool = True, sm_scale: float | None = None, out=None,
-                  stream=None) -> torch.Tensor:
+                  dedup: bool = True, sm_scale: float | None = None, path: str = "auto",
+                  out=None, stream=None) -> torch.Tensor:
     """Chunked-prefill attention of chunk `chunk` over a CFF-fused layer
     (kvf_chunk_prefill): q bf16 [B, chunk_blocks*t, Hq, d]
     attends to the keys of the earlier chunks and, causally, to its own chunk,
@@ -211,7 +211,7 @@ def chunk_prefill(q: torch.Tensor, state: FusionState, layer: int, B: int, p_blo
     N.call("kvf_chunk_prefill", N.ptr(q), N.ptr(state.pool_k), N.ptr(state.pool_v),
            dtype_code(state.pool_k.dtype), *g.args(), layer, N.ptr(state.table), N.ptr(state.k_scale),
            N.ptr(state.v_scale), N.ptr(order), B, p_blocks, chunk_blocks, chunk, Hq, float(sc),
-           1 if dedup else 0, N.ptr(out), N.stream_ptr(stream))
+           1 if dedup else 0, {"auto": 0, "mma": 1, "tc": 2}[path], N.ptr(out), N.stream_ptr(stream))
     return out
 
 

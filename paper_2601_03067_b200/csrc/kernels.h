@@ -203,6 +203,8 @@ struct ChunkPrefillArgs {
 };
 bool chunk_prefill_supported(const ChunkPrefillArgs& a, const char** why);
 cudaError_t launch_chunk_prefill(const ChunkPrefillArgs& a, cudaStream_t s);
+bool chunk_prefill_tc_supported(const ChunkPrefillArgs& a);  // kern_prefill_tc.cu
+cudaError_t launch_chunk_prefill_tc(const ChunkPrefillArgs& a, cudaStream_t s);
 
 // out[i] = map[ids[i]] for 0 <= ids[i] < map_len, else -1 (compaction: slot
 // tables / schedule ids -> dense rows of a compacted pool)

@@ -390,7 +390,8 @@ int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v, int
                       int64_t NB, int t, int h, int d, int head_mode, int64_t layer,
                       const int32_t* table, const void* k_scale, const void* v_scale,
                       const int32_t* order, int64_t B, int64_t p_blocks, int chunk_blocks,
-                      int chunk, int Hq, double sm_scale, int dedup, void* out, void* stream) {
+                      int chunk, int Hq, double sm_scale, int dedup, int path, void* out,
+                      void* stream) {
   ChunkPrefillArgs a;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
   if (dtype != BF16) return fail(KVF_ERR_INVALID, "chunked prefill needs bf16 pools");
@@ -417,6 +418,12 @@ int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v, int
   a.out = (float*)out;
   const char* why = "";
   if (!chunk_prefill_supported(a, &why)) return fail(KVF_ERR_INVALID, "chunked prefill: %s", why);
+  // path: 0 auto (= mma.sync: measured faster, 9.7 vs 10.1 ms on the last chunk of
+  // 4 x 16K), 1 mma.sync, 2 tcgen05 (S and P V in TMEM; softmax-warpgroup bound)
+  const bool tc_ok = chunk_prefill_tc_supported(a);
+  if (path == 2 && !tc_ok) return fail(KVF_ERR_INVALID, "tcgen05 chunked prefill needs d = 128, t = 16");
+  if (path == 2)
+    return cuda_status(launch_chunk_prefill_tc(a, (cudaStream_t)stream), "kvf_chunk_prefill[tc]");
   return cuda_status(launch_chunk_prefill(a, (cudaStream_t)stream), "kvf_chunk_prefill");
 }
 

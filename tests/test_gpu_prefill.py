@@ -40,8 +40,9 @@ def _reference(q, st, layer, B, p, chunk_blocks, chunk):
     return out
 
 
-@pytest.mark.parametrize("G,d", [(4, 128), (2, 64), (8, 128)])
-def test_chunk_prefill_vs_reference(G, d):
+@pytest.mark.parametrize("G,d,path", [(4, 128, "mma"), (2, 64, "mma"), (8, 128, "mma"),
+                                      (4, 128, "tc"), (8, 128, "tc"), (2, 128, "tc")])
+def test_chunk_prefill_vs_reference(G, d, path):
     L, B, p, t, h = 1, 2, 64, 16, 2
     chunk_blocks = 16
     Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=81, variant="cff")
@@ -54,7 +55,7 @@ def test_chunk_prefill_vs_reference(G, d):
     for chunk in range(p // chunk_blocks):
         q = torch.randn((B, chunk_blocks * t, Hq, d), device="cuda", dtype=torch.bfloat16)
         want = _reference(q, st, 0, B, p, chunk_blocks, chunk)
-        got = K.chunk_prefill(q, st, 0, B, p, chunk_blocks, chunk)
+        got = K.chunk_prefill(q, st, 0, B, p, chunk_blocks, chunk, path=path)
         torch.testing.assert_close(got.double(), want, atol=3e-3, rtol=3e-3)
-        slot = K.chunk_prefill(q, st, 0, B, p, chunk_blocks, chunk, dedup=False)
+        slot = K.chunk_prefill(q, st, 0, B, p, chunk_blocks, chunk, dedup=False, path=path)
         torch.testing.assert_close(got, slot, atol=2e-3, rtol=2e-3)

@@ -40,13 +40,14 @@ def timeit(fn, n=10):
 
 
 out = torch.empty((B, Tq, Hq, d), dtype=torch.float32, device="cuda")
-t_dedup = timeit(lambda: K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=True, out=out))
-t_slot = timeit(lambda: K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=False, out=out))
-a = K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=True)
-b = K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=False)
+PATH = os.environ.get("PATH_KIND", "auto")
+t_dedup = timeit(lambda: K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=True, out=out, path=PATH))
+t_slot = timeit(lambda: K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=False, out=out, path=PATH))
+a = K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=True, path=PATH)
+b = K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=False, path=PATH)
 tk = (chunk + 1) * Tq
 flops = 4.0 * B * Hq * Tq * (prev * t + Tq / 2) * d  # causal dense attention FLOPs
-line = (f"B={B} ctx={p * t} chunk={chunk} earlier slots {B * prev} -> unique blocks {uniq} "
+line = (f"path={PATH} B={B} ctx={p * t} chunk={chunk} earlier slots {B * prev} -> unique blocks {uniq} "
         f"(x{B * prev / uniq:.2f}); dense-equivalent {flops / 1e9:.0f} GFLOP\n"
         f"  chunk_prefill dedup    {t_dedup:7.3f} ms  ({flops / t_dedup / 1e9:6.0f} TFLOP/s dense-equivalent)\n"
         f"  chunk_prefill per-slot {t_slot:7.3f} ms  ({flops / t_slot / 1e9:6.0f} TFLOP/s)  speedup x{t_slot / t_dedup:.2f}"
