@@ -217,8 +217,9 @@ int kvf_paged_decode(const void* q, int q_dtype, const void* pool_k,
  * schedule's `order`). dedup = 1: S = Q K_P^T and P V_P once per physical
  * block P with the slots' scales folded in; dedup = 0: once per slot.
  * out: float32 [B][chunk_blocks*t][Hq][d]. bf16, folded, t = 16, Hq/h | 8.
- * path: 0 auto (mma.sync), 1 mma.sync kernel, 2 tcgen05 kernel (d = 128: S
- * and P V on the tensor cores, accumulators in TMEM, 4 units per softmax step). */
+ * path: 0 auto (tcgen05 when d = 128), 1 mma.sync kernel, 2 tcgen05 kernel
+ * (S and P V on the tensor cores, accumulators in TMEM, two query tiles per
+ * CTA, 4 units = 64 keys per softmax step). */
 int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v,
                       int dtype, int64_t L, int64_t NB, int t, int h, int d,
                       int head_mode, int64_t layer, const int32_t* table,

@@ -418,11 +418,11 @@ int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v, int
   a.out = (float*)out;
   const char* why = "";
   if (!chunk_prefill_supported(a, &why)) return fail(KVF_ERR_INVALID, "chunked prefill: %s", why);
-  // path: 0 auto (= mma.sync: measured faster, 9.7 vs 10.1 ms on the last chunk of
-  // 4 x 16K), 1 mma.sync, 2 tcgen05 (S and P V in TMEM; softmax-warpgroup bound)
+  // path: 0 auto (tcgen05 when the shape allows: 3.7 vs 9.7 ms mma.sync on the last
+  // chunk of 4 x 16K), 1 mma.sync, 2 tcgen05
   const bool tc_ok = chunk_prefill_tc_supported(a);
   if (path == 2 && !tc_ok) return fail(KVF_ERR_INVALID, "tcgen05 chunked prefill needs d = 128, t = 16");
-  if (path == 2)
+  if (path != 1 && tc_ok)
     return cuda_status(launch_chunk_prefill_tc(a, (cudaStream_t)stream), "kvf_chunk_prefill[tc]");
   return cuda_status(launch_chunk_prefill(a, (cudaStream_t)stream), "kvf_chunk_prefill");
 }
