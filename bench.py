@@ -494,12 +494,12 @@ def ours_main(args):
     torch.cuda.empty_cache()
     if rank == 0 and not args.skip_decode:
         out["decode"] = bench_decode(dev, torch)
-        if not args.skip_cpu:
+        if not args.skip_cpu and world == 1:
             try:
                 out["decode"]["cpu_baseline"] = run_cpu_decode_sample()
             except Exception as exc:  # reported, never fatal
                 out["decode"]["cpu_baseline"] = {"value": None, "error": str(exc)[-300:]}
-    if rank == 0 and not args.skip_cpu:
+    if rank == 0 and not args.skip_cpu and world == 1:  # the CPU baseline is an N = 1 figure
         try:
             s = run_cpu_sample(args.config, steps=2, warmup=1)
             v = s["bytes"] / statistics.mean(s["times"]) / 1e9
