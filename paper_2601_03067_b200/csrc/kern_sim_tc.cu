@@ -451,50 +451,101 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       // of near-threshold pairs to the exact float64 re-score (the tensor-core
       // fp32 accumulation over r/16 steps can be off by ~1e-4 relative)
       const float tlo = resc != nullptr ? thr - resc_band : thr;
+      // fast path in row-scaled space: t = acc * inv_j, s = inv_i * t (inv_i >= 0), so the
+      // row's sum / sum of squares / min / max of s follow from those of t; a column is a
+      // candidate when t clears a slightly lowered row threshold, and only candidate
+      // columns re-evaluate s exactly as below (bitwise the same decisions)
+      const float tcand = ok_i && inv_i > 0.f ? (tlo - 1e-5f) / inv_i : INFINITY;
+      float r1 = 0.f, r2 = 0.f, rmn = INFINITY, rmx = -INFINITY;
+      auto exact_chunk = [&](const uint32_t (&v)[32], int c0, unsigned okm, unsigned cols) {
+        unsigned hitm = 0;  // lane c: rows of this warp with a decided match in column c0 + c
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          if (!((cols >> c) & 1u)) continue;  // warp-uniform; static c keeps v in registers
+          const int col = c0 + c;
+          const bool ok = ok_i && ((okm >> c) & 1u);
+          const float sv = __uint_as_float(v[c]) * inv_i * inv_j[col];
+          bool hit = false;
+          if (ok && sv > tlo) {
+            hit = sv > thr;
+            if (resc != nullptr && fabsf(sv - thr) <= resc_band) {
+              const int pos = atomicAdd(resc_count, 1);
+              if (pos < resc_cap) {
+                int4 e;
+                e.x = (int)t.u;
+                e.y = my_id;
+                e.z = colid[col];
+                e.w = t.m;
+                reinterpret_cast<int4*>(resc)[pos] = e;
+                hit = false;  // decided by the re-score
+              }
+            }
+          }
+          const unsigned bb = __ballot_sync(0xffffffffu, hit);
+          if (lane == c) hitm = bb;
+        }
+        // first matching row of the warp per column (rows ascend with block id)
+        const int src = hitm ? __ffs(hitm) - 1 : 0;
+        const int32_t first = __shfl_sync(0xffffffffu, my_id, src);
+        if (hitm) atomicMin(&colmin[c0 + lane], first);
+      };
       for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
         // columns of this chunk that take part (alive, fusable, inside the merge)
         const unsigned okm = __ballot_sync(0xffffffffu, ok_j[c0 + lane] != 0);
         if (ok_i) cnt += (float)__popc(okm);
-        unsigned hitm = 0;  // lane c: rows of this warp with a decided match in column c0 + c
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const int col = c0 + c;
-          const bool ok = ok_i && ((okm >> c) & 1u);
-          const float s = __uint_as_float(v[c]) * inv_i * inv_j[col];
-          bool hit = false;
-          if (ok) {
-            s1 += s;
-            s2 = fmaf(s, s, s2);
-            mn = fminf(mn, s);
-            mx = fmaxf(mx, s);
-            if (s > tlo) {
-              hit = s > thr;
-              if (resc != nullptr && fabsf(s - thr) <= resc_band) {
-                const int pos = atomicAdd(resc_count, 1);
-                if (pos < resc_cap) {
-                  int4 e;
-                  e.x = (int)t.u;
-                  e.y = my_id;
-                  e.z = colid[col];
-                  e.w = t.m;
-                  reinterpret_cast<int4*>(resc)[pos] = e;
-                  hit = false;  // decided by the re-score
-                }
-              }
+        if (samp) {  // small runs that keep every sample: per-element reference path
+          for (int c = 0; c < 32; ++c) {
+            const int col = c0 + c;
+            const bool ok = ok_i && ((okm >> c) & 1u);
+            const float sv = __uint_as_float(v[c]) * inv_i * inv_j[col];
+            if (ok) {
+              s1 += sv;
+              s2 = fmaf(sv, sv, s2);
+              mn = fminf(mn, sv);
+              mx = fmaxf(mx, sv);
             }
+            if (row < ni && col < nj)
+              samp[(int64_t)(my_id - t.lb) * (t.re - t.mid) + (colid[col] - t.mid)] =
+                  ok ? (double)sv : (double)NAN;
           }
-          if (samp && row < ni && col < nj)
-            samp[(int64_t)(my_id - t.lb) * (t.re - t.mid) + (colid[col] - t.mid)] =
-                ok ? (double)s : (double)NAN;
-          const unsigned b = __ballot_sync(0xffffffffu, hit);
-          if (lane == c) hitm = b;
+          exact_chunk(v, c0, okm, 0xffffffffu);
+          continue;
         }
-        // first matching row of the warp per column (rows ascend with block id)
-        const int src = hitm ? __ffs(hitm) - 1 : 0;
-        const int32_t first = __shfl_sync(0xffffffffu, my_id, src);
-        if (hitm) atomicMin(&colmin[c0 + lane], first);
+        unsigned cand = 0;
+        if (okm == 0xffffffffu) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float tv = __uint_as_float(v[c]) * inv_j[c0 + c];
+            r1 += tv;
+            r2 = fmaf(tv, tv, r2);
+            rmn = fminf(rmn, tv);
+            rmx = fmaxf(rmx, tv);
+            cand |= (tv > tcand ? 1u : 0u) << c;
+          }
+        } else if (okm) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            if (!((okm >> c) & 1u)) continue;  // warp-uniform
+            const float tv = __uint_as_float(v[c]) * inv_j[c0 + c];
+            r1 += tv;
+            r2 = fmaf(tv, tv, r2);
+            rmn = fminf(rmn, tv);
+            rmx = fmaxf(rmx, tv);
+            cand |= (tv > tcand ? 1u : 0u) << c;
+          }
+        }
+        const unsigned cols = __reduce_or_sync(0xffffffffu, cand);
+        if (cols) exact_chunk(v, c0, okm, cols);
+      }
+      if (ok_i && !samp) {  // row moments back to similarity space
+        s1 += inv_i * r1;
+        s2 = fmaf(inv_i * inv_i, r2, s2);
+        if (rmn <= rmx) {
+          mn = fminf(mn, inv_i * rmn);
+          mx = fmaxf(mx, inv_i * rmx);
+        }
       }
       // accumulator drained: hand the buffer back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
