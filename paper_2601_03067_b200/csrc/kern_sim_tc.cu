@@ -43,6 +43,7 @@ constexpr int B_BYTES = BNH * BK * 2;  // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 512;  // two 256-column accumulators
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quarter, each half of the columns
+static_assert(kTcPartialsPerTile == 2 * EPI_WARPS, "one moment slot per epilogue warp of the pair");
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*meta*/;
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // cluster smem address of CTA 0
@@ -180,6 +181,27 @@ __device__ __forceinline__ TileInfo tile_info(int w, int nt, int64_t u0, const G
   return t;
 }
 
+// A published work item: w and the tile geometry (the scheduler warp computes it once,
+// consumers read it from shared memory instead of re-walking tiles / merges / rank)
+constexpr int kRec = 12;
+__device__ __forceinline__ TileInfo rec_info(const int32_t* r, int nt, int64_t u0) {
+  TileInfo t;
+  const int w = r[0];
+  t.ul = w / nt;
+  t.u = u0 + t.ul;
+  t.m = r[1];
+  t.i0 = r[2];
+  t.j0 = r[3];
+  t.lb = r[4];
+  t.mid = r[5];
+  t.re = r[6];
+  t.pl = r[7];
+  t.pm = r[8];
+  t.pr = r[9];
+  t.active = true;
+  return t;
+}
+
 __device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t cta) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
@@ -204,9 +226,10 @@ __device__ __forceinline__ void st_cluster_s32(const void* p, uint32_t cta, int3
 }
 
 constexpr int SCHED_DEPTH = 4;
-// sched_empty arrivals per slot: leader MMA warp + peer producer + EPI_WARPS epilogue
+// sched_empty arrivals per slot: producers of both CTAs + leader MMA warp + the
+// epilogue warps of both CTAs
 // warps in each CTA
-constexpr uint32_t kSchedConsumers = 2 + 2 * EPI_WARPS;
+constexpr uint32_t kSchedConsumers = 3 + 2 * EPI_WARPS;
 
 // Persistent: P CTA pairs pull work items from a global counter (the leader's
 // producer thread fetches, skips tiles beyond the alive blocks, and broadcasts
@@ -232,13 +255,13 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   uint64_t* tmem_empty = tmem_full + 2;               // [2], used on the leader
   uint64_t* sched_full = tmem_empty + 2;              // [SCHED_DEPTH]
   uint64_t* sched_empty = sched_full + SCHED_DEPTH;   // [SCHED_DEPTH], used on the leader
-  int32_t* sched_w = reinterpret_cast<int32_t*>(sched_empty + SCHED_DEPTH);  // [SCHED_DEPTH]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_w + SCHED_DEPTH);
-  float* inv_j = reinterpret_cast<float*>(meta + 512);
-  int32_t* colmin = reinterpret_cast<int32_t*>(meta + 512 + 4 * BN);
-  uint8_t* ok_j = meta + 512 + 8 * BN;
-  double* red = reinterpret_cast<double*>(meta + 512 + 9 * BN);            // 8 warps x 5
-  int32_t* colid = reinterpret_cast<int32_t*>(meta + 512 + 9 * BN + 512);  // block ids
+  int32_t* sched_rec = reinterpret_cast<int32_t*>(sched_empty + SCHED_DEPTH);  // [SCHED_DEPTH][kRec]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_rec + SCHED_DEPTH * kRec);
+  // epilogue column metadata, double-buffered by tile parity: [2][BN] each
+  float* inv_j_b = reinterpret_cast<float*>(meta + 512);
+  int32_t* colmin_b = reinterpret_cast<int32_t*>(meta + 512 + 8 * BN);
+  int32_t* colid_b = reinterpret_cast<int32_t*>(meta + 512 + 16 * BN);  // block ids
+  uint8_t* ok_j_b = meta + 512 + 24 * BN;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
@@ -259,6 +282,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
     }
+    for (int c = 0; c < 2 * BN; ++c) colmin_b[c] = kNone;
     for (int b = 0; b < SCHED_DEPTH; ++b) {
       mbar_init(&sched_full[b], 1);
       mbar_init(&sched_empty[b], kSchedConsumers);
@@ -288,38 +312,17 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const uint32_t sph = (it / SCHED_DEPTH) & 1;
       int w = 0;
       if (lane == 0) {
-        if (leader) {  // fetch the next tile with alive blocks; publish it to both CTAs
-          mbar_wait_cluster(&sched_empty[sl], sph ^ 1);
-          for (;;) {
-            w = atomicAdd(work_counter, 1);
-            if (w >= nwork) {
-              if (w == nwork + P - 1) atomicExch(work_counter, 0);  // last fetch of the launch
-              w = -1;
-              break;
-            }
-            const TileInfo t0 = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
-            if (t0.active) break;
-            const int tile = w - (int)t0.ul * nt;  // tile fully beyond the alive blocks
-            double* pp = partials + ((int64_t)t0.ul * 2 * nt + 2 * tile) * 5;
-            for (int q = 0; q < 2; ++q) {
-              pp[5 * q + 0] = pp[5 * q + 1] = pp[5 * q + 2] = 0.0;
-              pp[5 * q + 3] = INFINITY;
-              pp[5 * q + 4] = -INFINITY;
-            }
-          }
-          sched_w[sl] = w;
-          st_cluster_s32(&sched_w[sl], 1, w);
-          mbar_arrive_cluster(&sched_full[sl], 0);
-          mbar_arrive_cluster(&sched_full[sl], 1);
-        } else {
-          mbar_wait_cluster(&sched_full[sl], sph);
-          w = sched_w[sl];
-          mbar_arrive_cluster(&sched_empty[sl], 0);
-        }
+        mbar_wait_cluster(&sched_full[sl], sph);
+        w = sched_rec[sl * kRec];
       }
       w = __shfl_sync(0xffffffffu, w, 0);
-      if (w < 0) break;
-      const TileInfo t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+      if (w < 0) {
+        if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
+        break;
+      }
+      const TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
       const int layer = (int)(t.u / layer_div);
       const int head = g.head_mode ? (int)(t.u % g.h) : 0;
       const int mi0 = t.i0 + (int)crank * BM;
@@ -374,13 +377,55 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
       }
     }
+  } else if (warp == 3) {
+    // tile scheduler (leader CTA): fetch the next work item with alive blocks,
+    // resolve its geometry, publish the record to both CTAs, SCHED_DEPTH ahead
+    if (leader && lane == 0) {
+      for (uint32_t it = 0;; ++it) {
+        const int sl = it % SCHED_DEPTH;
+        mbar_wait_cluster(&sched_empty[sl], ((it / SCHED_DEPTH) & 1) ^ 1);
+        int w;
+        TileInfo t0;
+        for (;;) {
+          w = atomicAdd(work_counter, 1);
+          if (w >= nwork) {
+            if (w == nwork + P - 1) atomicExch(work_counter, 0);  // last fetch of the launch
+            w = -1;
+            break;
+          }
+          t0 = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+          if (t0.active) break;
+          const int tile = w - (int)t0.ul * nt;  // tile fully beyond the alive blocks
+          double* pp = partials + ((int64_t)t0.ul * nt + tile) * kTcPartialsPerTile * 5;
+          for (int q = 0; q < kTcPartialsPerTile; ++q) {
+            pp[5 * q + 0] = pp[5 * q + 1] = pp[5 * q + 2] = 0.0;
+            pp[5 * q + 3] = INFINITY;
+            pp[5 * q + 4] = -INFINITY;
+          }
+        }
+        int32_t r[kRec] = {w, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (w >= 0) {
+          r[1] = t0.m; r[2] = t0.i0; r[3] = t0.j0; r[4] = t0.lb; r[5] = t0.mid; r[6] = t0.re;
+          r[7] = t0.pl; r[8] = t0.pm; r[9] = t0.pr;
+        }
+        int32_t* dst = sched_rec + sl * kRec;
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+          dst[q] = r[q];
+          st_cluster_s32(dst + q, 1, r[q]);
+        }
+        mbar_arrive_cluster(&sched_full[sl], 0);
+        mbar_arrive_cluster(&sched_full[sl], 1);
+        if (w < 0) break;
+      }
+    }
   } else if (warp == 1) {
     if (leader && lane == 0) {
       uint32_t kk = 0, tc = 0;
       for (uint32_t it = 0;; ++it) {
         const int sl = it % SCHED_DEPTH;
         mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
-        const int w = sched_w[sl];
+        const int w = sched_rec[sl * kRec];
         mbar_arrive_cluster(&sched_empty[sl], 0);
         if (w < 0) break;
         const uint32_t acc = tc & 1;
@@ -404,23 +449,44 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       }
     }
   } else if (warp >= 4) {
+    // Epilogue. Column metadata (inverse norms, masks, block ids) and the per-column
+    // first-match minima are double-buffered by tile parity, so a tile needs one
+    // barrier (its metadata is written); the minima of tile k are flushed to the
+    // global absorbers after tile k+1's barrier (every warp is past tile k then),
+    // and each warp writes its own moment slot (reduced in fixed order by
+    // level_stats), so no warp waits for another at the end of a tile.
     const int ew = warp - 4;
     const int quarter = ew & 3;           // TMEM lanes [32*quarter, 32*quarter + 32)
     const int col0 = (ew >> 2) * (BN / 2);  // this warp's half of the columns
     const int row = quarter * 32 + lane;
     const int et = threadIdx.x - 128;
     constexpr int ET = 32 * EPI_WARPS;
+    static_assert(ET >= BN, "one epilogue thread per column for the flush");
     uint32_t tc = 0;
+    int64_t prev_gb = -1;  // unit base of the tile whose minima are pending
+    auto flush = [&](int buf) {  // thread et owns column et of buffer buf
+      if (et < BN && prev_gb >= 0) {
+        int32_t* cmin = colmin_b + buf * BN;
+        const int32_t cm = cmin[et];
+        if (cm != kNone) atomicMin(&absorber[prev_gb + colid_b[buf * BN + et]], cm);
+        cmin[et] = kNone;
+      }
+    };
     for (uint32_t it = 0;; ++it) {
       const int sl = it % SCHED_DEPTH;
       mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
-      const int w = sched_w[sl];
+      const int w = sched_rec[sl * kRec];
+      const TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
       if (w < 0) break;
-      const TileInfo t = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+      const int mb = (int)(tc & 1);  // metadata buffer of this tile
+      float* inv_j = inv_j_b + mb * BN;
+      int32_t* colmin = colmin_b + mb * BN;
+      uint8_t* ok_j = ok_j_b + mb * BN;
+      int32_t* colid = colid_b + mb * BN;
       const int tile = w - (int)t.ul * nt;
-      double* pp = partials + ((int64_t)t.ul * 2 * nt + 2 * tile + crank) * 5;
+      double* pp = partials + (((int64_t)t.ul * nt + tile) * kTcPartialsPerTile + crank * EPI_WARPS + ew) * 5;
       const int64_t gb = t.u * g.NB;
       const int32_t* lv = live + gb;
       const int mi0 = t.i0 + (int)crank * BM;
@@ -428,21 +494,28 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int nj = min(BN, t.pr - t.pm - t.j0);
       for (int c = et; c < BN; c += ET) {  // column metadata
         const int64_t bj = gb + (c < nj ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
-        const bool ok = c < nj && alive[bj] && fusable[bj];
+        // independent loads (one round trip), combined afterwards
+        const uint8_t al = alive[bj], fu = fusable[bj];
+        const float nk = knorm[bj];
+        const bool ok = c < nj && al && fu;
         colid[c] = (int32_t)(bj - gb);
-        const float nv = ok ? knorm[bj] : 0.f;
+        const float nv = ok ? nk : 0.f;
         ok_j[c] = ok;
         inv_j[c] = nv > 0.f ? 1.f / nv : 0.f;
-        colmin[c] = kNone;
       }
       const int32_t my_id = row < ni ? (staged ? lv[t.pl + mi0 + row] : t.lb + mi0 + row) : 0;
       const int64_t bi = gb + my_id;
-      const bool ok_i = row < ni && alive[bi] && fusable[bi];
-      const float ni_v = ok_i ? knorm[bi] : 0.f;
+      const uint8_t al_i = alive[bi], fu_i = fusable[bi];
+      const float nk_i = knorm[bi];
+      const bool ok_i = row < ni && al_i && fu_i;
+      const float ni_v = ok_i ? nk_i : 0.f;
       const float inv_i = ni_v > 0.f ? 1.f / ni_v : 0.f;
-      float cnt = 0.f, s1 = 0.f, s2 = 0.f, mn = INFINITY, mx = -INFINITY;
+      float s1 = 0.f, s2 = 0.f, mn = INFINITY, mx = -INFINITY;
+      int cnt = 0;
       double* samp = samples ? samples + t.ul * sample_stride + sample_off[t.m] : nullptr;
       asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");  // column metadata visible
+      flush(mb ^ 1);  // the previous tile's first matches (every warp is past it)
+      prev_gb = gb;
 
       const uint32_t acc = tc & 1;
       mbar_wait(&tmem_full[acc], (tc >> 1) & 1);
@@ -457,44 +530,38 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       // columns re-evaluate s exactly as below (bitwise the same decisions)
       const float tcand = ok_i && inv_i > 0.f ? (tlo - 1e-5f) / inv_i : INFINITY;
       float r1 = 0.f, r2 = 0.f, rmn = INFINITY, rmx = -INFINITY;
-      auto exact_chunk = [&](const uint32_t (&v)[32], int c0, unsigned okm, unsigned cols) {
-        unsigned hitm = 0;  // lane c: rows of this warp with a decided match in column c0 + c
+      // exact decisions for this thread's candidate columns (bit c of `cols`): no warp
+      // collectives; a match lowers the column's first matching row in shared memory
+      auto exact_cols = [&](const uint32_t (&v)[32], int c0, unsigned okm, unsigned cols) {
 #pragma unroll
         for (int c = 0; c < 32; ++c) {
-          if (!((cols >> c) & 1u)) continue;  // warp-uniform; static c keeps v in registers
+          if (!((cols >> c) & 1u)) continue;  // static c keeps v in registers
           const int col = c0 + c;
-          const bool ok = ok_i && ((okm >> c) & 1u);
+          if (!(ok_i && ((okm >> c) & 1u))) continue;
           const float sv = __uint_as_float(v[c]) * inv_i * inv_j[col];
-          bool hit = false;
-          if (ok && sv > tlo) {
-            hit = sv > thr;
-            if (resc != nullptr && fabsf(sv - thr) <= resc_band) {
-              const int pos = atomicAdd(resc_count, 1);
-              if (pos < resc_cap) {
-                int4 e;
-                e.x = (int)t.u;
-                e.y = my_id;
-                e.z = colid[col];
-                e.w = t.m;
-                reinterpret_cast<int4*>(resc)[pos] = e;
-                hit = false;  // decided by the re-score
-              }
+          if (!(sv > tlo)) continue;
+          bool hit = sv > thr;
+          if (resc != nullptr && fabsf(sv - thr) <= resc_band) {
+            const int pos = atomicAdd(resc_count, 1);
+            if (pos < resc_cap) {
+              int4 e;
+              e.x = (int)t.u;
+              e.y = my_id;
+              e.z = colid[col];
+              e.w = t.m;
+              reinterpret_cast<int4*>(resc)[pos] = e;
+              hit = false;  // decided by the re-score
             }
           }
-          const unsigned bb = __ballot_sync(0xffffffffu, hit);
-          if (lane == c) hitm = bb;
+          if (hit) atomicMin(&colmin[col], my_id);
         }
-        // first matching row of the warp per column (rows ascend with block id)
-        const int src = hitm ? __ffs(hitm) - 1 : 0;
-        const int32_t first = __shfl_sync(0xffffffffu, my_id, src);
-        if (hitm) atomicMin(&colmin[c0 + lane], first);
       };
       for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
         // columns of this chunk that take part (alive, fusable, inside the merge)
         const unsigned okm = __ballot_sync(0xffffffffu, ok_j[c0 + lane] != 0);
-        if (ok_i) cnt += (float)__popc(okm);
+        if (ok_i) cnt += __popc(okm);
         if (samp) {  // small runs that keep every sample: per-element reference path
           for (int c = 0; c < 32; ++c) {
             const int col = c0 + c;
@@ -510,7 +577,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               samp[(int64_t)(my_id - t.lb) * (t.re - t.mid) + (colid[col] - t.mid)] =
                   ok ? (double)sv : (double)NAN;
           }
-          exact_chunk(v, c0, okm, 0xffffffffu);
+          exact_cols(v, c0, okm, 0xffffffffu);
           continue;
         }
         unsigned cand = 0;
@@ -536,8 +603,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
             cand |= (tv > tcand ? 1u : 0u) << c;
           }
         }
-        const unsigned cols = __reduce_or_sync(0xffffffffu, cand);
-        if (cols) exact_chunk(v, c0, okm, cols);
+        if (cand) exact_cols(v, c0, okm, cand);
       }
       if (ok_i && !samp) {  // row moments back to similarity space
         s1 += inv_i * r1;
@@ -552,41 +618,25 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
       ++tc;
-      // per-CTA similarity moments: deterministic warp tree, then fixed warp order
-      double dc = cnt, d1 = s1, d2 = s2, dmn = mn, dmx = mx;
+      // this warp's similarity moments -> its own slot (fp32 warp tree, fixed order)
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        dc += __shfl_xor_sync(0xffffffffu, dc, o);
-        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
-        d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-        dmn = fmin(dmn, __shfl_xor_sync(0xffffffffu, dmn, o));
-        dmx = fmax(dmx, __shfl_xor_sync(0xffffffffu, dmx, o));
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       }
       if (lane == 0) {
-        red[ew * 5 + 0] = dc;
-        red[ew * 5 + 1] = d1;
-        red[ew * 5 + 2] = d2;
-        red[ew * 5 + 3] = dmn;
-        red[ew * 5 + 4] = dmx;
+        pp[0] = (double)cnt;
+        pp[1] = (double)s1;
+        pp[2] = (double)s2;
+        pp[3] = (double)mn;
+        pp[4] = (double)mx;
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");
-      for (int c = et; c < BN; c += ET) {
-        const int32_t cm = colmin[c];
-        if (cm != kNone) atomicMin(&absorber[gb + colid[c]], cm);
-      }
-      if (et == 0) {
-        double o[5] = {0, 0, 0, INFINITY, -INFINITY};
-        for (int q = 0; q < EPI_WARPS; ++q) {
-          o[0] += red[q * 5 + 0];
-          o[1] += red[q * 5 + 1];
-          o[2] += red[q * 5 + 2];
-          o[3] = fmin(o[3], red[q * 5 + 3]);
-          o[4] = fmax(o[4], red[q * 5 + 4]);
-        }
-        for (int q = 0; q < 5; ++q) pp[q] = o[q];
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");  // metadata free for the next tile
     }
+    asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");  // every warp past the last tile
+    flush((int)((tc & 1) ^ 1));
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -69,7 +69,7 @@ cudaError_t launch_sim_simt(const SimArgs& a, cudaStream_t s);
 // similarity partials written per CTA (2 slots per tile)
 constexpr int kTcTileM = 256;
 constexpr int kTcTileN = 256;
-constexpr int kTcPartialsPerTile = 2;
+constexpr int kTcPartialsPerTile = 16;  // one moment slot per epilogue warp of the CTA pair
 bool tc_supported(const SimArgs& a, const char** why);
 cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s);
 

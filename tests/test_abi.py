@@ -52,7 +52,7 @@ def test_argument_errors_map_to_reference_exceptions():
     assert rc == N.KVF_ERR_INVALID
     tm, tn, ppt = C.c_int(), C.c_int(), C.c_int()
     assert lib.kvf_sim_tile_shape(2, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
-    assert (tm.value, tn.value, ppt.value) == (256, 256, 2)
+    assert (tm.value, tn.value, ppt.value) == (256, 256, 16)  # one moment slot per epilogue warp
     assert lib.kvf_sim_tile_shape(1, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) != 0
 
 
