@@ -6,6 +6,7 @@
 //   K5  table remap/refcounts  (core.py:217-227, fusion.py:262-264)
 //   --  finalize: per-slot scales, live/free lists (fusion.py:316-324)
 //   --  audit / redirect / gather / refold (core.py:232-241, 285-305)
+#include <type_traits>
 #include "kernels.h"
 #include "vec_io.cuh"
 
@@ -67,11 +68,92 @@ __global__ void block_norms_kernel(const T* __restrict__ pool, Geom g,
   if (lane == 0) norms[w] = sqrt(acc);
 }
 
+// Per-head units, bf16, d = 128, h = 8: one warp per physical block reads the block's
+// contiguous 32 KB (a per-head warp would read 16 rows of 256 B at a 2 KB stride, and
+// the eight heads' passes would reopen every DRAM page 8 times). A 512-B warp step
+// covers two (token, head) rows: lanes 0-15 even heads, 16-31 odd heads, so step k of
+// a lane adds to head 2 (k % 4) + lane / 16 -- four accumulators with static indices.
+__global__ void block_norms_heads_kernel(const __nv_bfloat16* __restrict__ pool, Geom g,
+                                         float* __restrict__ norms) {
+  constexpr int D = 128, H = 8, T = 16;
+  const int64_t nblk = g.L * g.NB;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nblk) return;
+  const uint4* base = reinterpret_cast<const uint4*>(pool + w * (int64_t)(T * H * D));
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+  for (int k = 0; k < T * H * D / 8 / 32; ++k) {  // 64 steps of 32 x 16 B
+    const uint4 q = __ldg(base + k * 32 + lane);
+    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+    float a = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(p2[e]);
+      a = fmaf(f.x, f.x, a);
+      a = fmaf(f.y, f.y, a);
+    }
+    acc[k & 3] += a;
+  }
+  const int64_t layer = w / g.NB, blk = w % g.NB;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    float v = acc[j];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // within 16 lanes
+    if ((lane & 15) == 0) {
+      const int head = 2 * j + (lane >> 4);
+      norms[(layer * H + head) * g.NB + blk] = sqrtf(v);
+    }
+  }
+}
+
+// Folded units, bf16: warp per block over its contiguous E elements, four independent
+// 16-B loads in flight per lane (the generic loop above keeps one)
+__global__ void block_norms_flat_kernel(const __nv_bfloat16* __restrict__ pool, int64_t nvec,
+                                        int64_t E, float* __restrict__ norms) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nvec) return;
+  const uint4* base = reinterpret_cast<const uint4*>(pool + w * E);
+  const int64_t nch = E / 8;
+  float acc = 0.f;
+#pragma unroll 4
+  for (int64_t c = lane; c < nch; c += 32) {
+    const uint4 q = __ldg(base + c);
+    const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&q);
+    float a = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(p2[e]);
+      a = fmaf(f.x, f.x, a);
+      a = fmaf(f.y, f.y, a);
+    }
+    acc += a;
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) norms[w] = sqrtf(acc);
+}
+
 template <typename T>
 static cudaError_t norms_t(const void* pool, const Geom& g, void* norms, cudaStream_t s) {
   using A = typename AccOf<T>::type;
   const int64_t nvec = g.units() * g.NB;
   const int64_t blocks = (nvec * 32 + 255) / 256;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (g.head_mode && g.d == 128 && g.h == 8 && g.t == 16 &&
+        (reinterpret_cast<uintptr_t>(pool) & 15) == 0) {
+      const int64_t nblk = g.L * g.NB;
+      block_norms_heads_kernel<<<(unsigned)((nblk * 32 + 255) / 256), 256, 0, s>>>(
+          (const __nv_bfloat16*)pool, g, (float*)norms);
+      return cudaGetLastError();
+    }
+    if (!g.head_mode && g.E() % 8 == 0 && (reinterpret_cast<uintptr_t>(pool) & 15) == 0) {
+      block_norms_flat_kernel<<<(unsigned)blocks, 256, 0, s>>>((const __nv_bfloat16*)pool, nvec, g.E(),
+                                                               (float*)norms);
+      return cudaGetLastError();
+    }
+  }
   if (can_vectorize<T>(pool, g))
     block_norms_kernel<T, Vec16<T>::N><<<(unsigned)blocks, 256, 0, s>>>((const T*)pool, g, (A*)norms);
   else
