@@ -582,6 +582,166 @@ merge_warp_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// K4 for short vectors (per-head units, bf16): warp per item with a per-warp
+// shared-memory ring. The item loop of merge_warp_kernel keeps one vector in
+// flight per warp (its registers hold the accumulators); here NS - 1 member
+// vectors stream into the ring by bulk copies (one per token row, issued by t
+// lanes in parallel) while the warp accumulates the current one, running
+// across item boundaries. Slot metadata (1/norm, item id, last flag) travels
+// with the slot, so the consuming side never looks an item up.
+// ---------------------------------------------------------------------------
+struct RingSlotMeta {
+  float inv, home;
+  int32_t gid, flags;  // flags: bit0 last vector of the item, bit1 V tensor
+};
+template <int CPL, int NS>
+__global__ void __launch_bounds__(256, 2)
+merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict__ pool_v, Geom g,
+                  float* __restrict__ knorm, float* __restrict__ vnorm,
+                  const float* __restrict__ oknorm, const float* __restrict__ ovnorm,
+                  int32_t* ws, int64_t n_total) {
+  constexpr int VB = CPL * 512;  // vector bytes (32 lanes x CPL x 16 B)
+  extern __shared__ __align__(128) uint8_t rsm[];
+  const LevelWs W(ws, n_total);
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = rsm + (size_t)wl * NS * VB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rsm + (size_t)(blockDim.x >> 5) * NS * VB) + wl * NS;
+  RingSlotMeta* smeta = reinterpret_cast<RingSlotMeta*>(
+                            reinterpret_cast<uint64_t*>(rsm + (size_t)(blockDim.x >> 5) * NS * VB) +
+                            (blockDim.x >> 5) * NS) + wl * NS;
+  if (lane == 0)
+    for (int q = 0; q < NS; ++q) mbar_init(&bars[q], 1);
+  __syncwarp();
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t n_items = 2 * (int64_t)(*W.count);
+  const uint32_t segb = (uint32_t)(g.d * 2);
+  const int64_t rstride = (int64_t)g.h * g.d;  // elements between token rows
+
+  // ---- issue side: item it_i, vector v_i; lane k holds vector k's id and 1/norm ----
+  int64_t it_i = gw;
+  int v_i = 0, n_i = 0, s0_i = 0;
+  int64_t gid_i = 0;
+  int32_t id_l = 0;
+  float inv_l = 0.f, home_i = 0.f;
+  auto load_item = [&]() {  // all lanes
+    if (it_i >= n_items) return;
+    const bool is_v = it_i & 1;
+    const float* norm = is_v ? vnorm : knorm;
+    gid_i = W.list[it_i >> 1];
+    n_i = W.mcnt[gid_i];
+    s0_i = W.mstart[gid_i];
+    home_i = (is_v ? ovnorm : oknorm)[gid_i];
+    const int64_t gb = (gid_i / g.NB) * g.NB;
+    id_l = (int32_t)(gid_i - gb);
+    inv_l = 0.f;
+    if (lane <= n_i) {
+      if (lane > 0) id_l = W.members[s0_i + lane - 1];
+      const float nv = norm[gb + id_l];
+      inv_l = nv > 0.f ? 1.f / nv : 0.f;
+    }
+  };
+  uint32_t q_i = 0, q_c = 0;
+  auto issue = [&]() {  // all lanes
+    if (it_i >= n_items) return;
+    const bool is_v = it_i & 1;
+    int32_t id;
+    float inv;
+    if (v_i < 32) {
+      id = __shfl_sync(0xffffffffu, id_l, v_i);
+      inv = __shfl_sync(0xffffffffu, inv_l, v_i);
+    } else {  // groups beyond one warp of members
+      const int64_t gb = (gid_i / g.NB) * g.NB;
+      id = W.members[s0_i + v_i - 1];
+      const float nv = (is_v ? vnorm : knorm)[gb + id];
+      inv = nv > 0.f ? 1.f / nv : 0.f;
+    }
+    const int s = q_i % NS;
+    const int64_t u = gid_i / g.NB;
+    if (lane == 0) {
+      RingSlotMeta m;
+      m.inv = inv;
+      m.home = home_i;
+      m.gid = (int32_t)gid_i;
+      m.flags = (v_i == n_i ? 1 : 0) | (is_v ? 2 : 0);
+      smeta[s] = m;
+      mbar_expect_tx(&bars[s], (uint32_t)VB);  // release: slot meta visible after the wait
+    }
+    __syncwarp();
+    if (lane < g.t) {
+      const __nv_bfloat16* src = (is_v ? pool_v : pool_k) + g.base(u, id) + lane * rstride;
+      bulk_g2s(ring + (size_t)s * VB + lane * segb, src, segb, &bars[s]);
+    }
+    ++q_i;
+    if (++v_i > n_i) {
+      v_i = 0;
+      it_i += nw;
+      load_item();
+    }
+  };
+
+  load_item();
+  for (int k = 0; k < NS - 1; ++k) issue();
+  float acc[CPL][8];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
+  for (int64_t it = gw; it < n_items;) {
+    issue();
+    const int s = q_c % NS;
+    mbar_wait(&bars[s], (q_c / NS) & 1);
+    const RingSlotMeta m = smeta[s];
+    const uint4* sp = reinterpret_cast<const uint4*>(ring + (size_t)s * VB);
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const uint4 raw = sp[q * 32 + lane];
+      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(p2[e]);
+        acc[q][2 * e] = fmaf(f.x, m.inv, acc[q][2 * e]);
+        acc[q][2 * e + 1] = fmaf(f.y, m.inv, acc[q][2 * e + 1]);
+      }
+    }
+    __syncwarp();  // the slot may be refilled by the next issue
+    ++q_c;
+    if (!(m.flags & 1)) continue;
+    // item complete: x_l <- home * unit(sum), stored norm of the written bf16 vector
+    const bool is_v = m.flags & 2;
+    __nv_bfloat16* pool = is_v ? pool_v : pool_k;
+    float* norm = is_v ? vnorm : knorm;
+    float ss = 0.f;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ss = fmaf(acc[q][e], acc[q][e], ss);
+    const float nrm = sqrtf(warp_sum(ss));
+    const float sc = nrm > 0.f ? (m.home > 0.f ? m.home : 1.f) / nrm : 0.f;
+    const int64_t u = m.gid / g.NB;
+    const int32_t l = (int32_t)(m.gid % g.NB);
+    __nv_bfloat16* xl = pool + g.base(u, l);
+    float rs = 0.f;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      float yv[8], rd[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) yv[e] = acc[q][e] * sc;
+      VecIO<__nv_bfloat16, 8>::store(xl + g.off((int64_t)(q * 32 + lane) * 8), yv, rd);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        rs = fmaf(rd[e], rd[e], rs);
+        acc[q][e] = 0.f;
+      }
+    }
+    rs = warp_sum(rs);
+    if (lane == 0) norm[m.gid] = sqrtf(rs);
+    it += nw;
+  }
+}
+
 namespace {
 template <typename T, int VEC>
 cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
@@ -642,6 +802,28 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
   const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    // per-head units of 4 KB: warp per item, per-warp smem ring (3 slots)
+    if (g.head_mode && vbytes == 4096 && g.t <= 32 && (g.d * 2) % 16 == 0 && can_vectorize<T>(pk, g) &&
+        can_vectorize<T>(pv, g) && !getenv("KVF_MERGE_NO_RING")) {
+      auto go = [&](auto kern, int ns, int wpb, int per_sm) {
+        const int smem = wpb * ns * 4096 + wpb * ns * (8 + (int)sizeof(RingSlotMeta));
+        static bool attr = false;
+        if (!attr) {
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+          if (e != cudaSuccess) return e;
+          attr = true;
+        }
+        kern<<<148 * per_sm, wpb * 32, smem, s>>>((__nv_bfloat16*)pk, (__nv_bfloat16*)pv, g, (float*)kn,
+                                                  (float*)vn, (const float*)okn, (const float*)ovn, ws,
+                                                  n_total);
+        return cudaGetLastError();
+      };
+      // measured (cfg2 per-head, 2 steps): 8 warps x 3 slots x 2 CTAs/SM 23.6 ms; 6 x 4 x 2 28.6;
+      // 4 x 5 x 3 51.2; 8 x 3 x 1 41.1 (merge_warp_kernel: 28.2)
+      return go(merge_ring_kernel<8, 3>, 3, 8, 2);
+    }
+  }
   if constexpr (!std::is_same<T, double>::value) {
     // short vectors (per-head units): warp per item
     const bool vec_ok = can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g);
