@@ -125,7 +125,36 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: KVF_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 (multi-rank smoke test of
+    # the bench's distributed logic on one GPU, with KVF_BENCH_BACKEND=gloo)
+    if os.environ.get("KVF_BENCH_ONE_DEVICE") == "1":
+        local = 0
     return world, rank, local
+
+
+def dist_backend():
+    return os.environ.get("KVF_BENCH_BACKEND", "nccl")
+
+
+def reduce_max(dist, t):
+    """In-place MAX over ranks (the gloo test hook reduces a host copy)."""
+    if dist_backend() == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    else:
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.MAX)
+        t.copy_(h)
+
+
+def all_gather_rows(dist, out, mine):
+    """out[r] = rank r's `mine` (NCCL: one all_gather_into_tensor; gloo test hook: lists)."""
+    if dist_backend() == "nccl":
+        dist.all_gather_into_tensor(out, mine)
+    else:
+        parts = [t.cpu() for t in out.unbind(0)]
+        dist.all_gather(parts, mine.cpu())
+        for r, t in enumerate(parts):
+            out[r].copy_(t)
 
 
 def kv_bytes(c, elem):
@@ -324,7 +353,7 @@ def ours_main(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(dist_backend(), device_id=dev if dist_backend() == "nccl" else None)
     c = CONFIGS[args.config]
     dtype = torch.bfloat16 if c["dtype"] == "bf16" else torch.float32
     elem = 2 if dtype == torch.bfloat16 else 4
@@ -364,7 +393,7 @@ def ours_main(args):
         else:
             st = engine.run(Kw.view(-1), Vw.view(-1), c["thr"], time_sim=timed)
         if world > 1:  # the path's only collective: gather per-unit block counts
-            dist.all_gather_into_tensor(gathered, st.live_count)
+            all_gather_rows(dist, gathered, st.live_count)
         else:
             gathered[0].copy_(st.live_count)
         e1.record()
@@ -415,7 +444,7 @@ def ours_main(args):
     flops *= len(recs) / len(sim_recs)
     tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        reduce_max(dist, tmax)
     total_ms = float(tmax.item())
     ms_per_step = total_ms / args.steps
     live = gathered.sum().item()
@@ -719,7 +748,7 @@ def bench_e2e(args, c, K0, V0, dtype, dev, world, torch, dist, PagedKvCache, Cac
     torch.cuda.synchronize()
     dt = torch.tensor([(time.perf_counter() - t0) / steps], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        reduce_max(dist, dt)
     per = float(dt.item())
     elem = 2 if dtype == torch.bfloat16 else 4
     return {"value": world * kv_bytes(c, elem) / per / 1e9, "unit": "GB/s",
@@ -750,7 +779,7 @@ def ours_cfg5(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(dist_backend(), device_id=dev if dist_backend() == "nccl" else None)
     c = CONFIGS["cfg5"]
     L, B, p, t, h, d = c["L"], c["B"], c["p"], c["t"], c["h"], c["d"]
     mine = list(shard_units(L, world, rank))
@@ -781,7 +810,7 @@ def ours_cfg5(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if world > 1:
-            dist.all_gather_into_tensor(gathered, live)
+            all_gather_rows(dist, gathered, live)
         else:
             gathered[0].copy_(live)
         e1.record()
@@ -806,7 +835,7 @@ def ours_cfg5(args):
     ms_step = sum(r[0] for r in res) / args.steps * scale
     tmax = torch.tensor([ms_step], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        reduce_max(dist, tmax)
     ms_step = float(tmax.item())
     sim_ms = sum(r[1] for r in res)
     flops = sum(r[2] for r in res)
