@@ -69,8 +69,9 @@ def _cache(L, B, p, t, h, d, dtype, seed, variant="bff"):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
 @pytest.mark.parametrize("head_mode", ["folded", "per_head"])
 @pytest.mark.parametrize("thr", [0.8, 0.7])
-def test_bff_vs_oracle(dtype, head_mode, thr):
-    L, B, p, t, h, d = 2, 8, 16, 16, 2, 64
+@pytest.mark.parametrize("d", [64, 128])  # d = 128: Llama head dim (4 KB per-head vectors)
+def test_bff_vs_oracle(dtype, head_mode, thr, d):
+    L, B, p, t, h = 2, 8, 16, 16, 2
     cache, Kh, Vh = _cache(L, B, p, t, h, d, dtype, seed=11)
     outs = K.fuse_batch(cache, K.FusionConfig(threshold=thr, head_mode=head_mode), keep_samples=True)
     assert len(outs) == (L * h if head_mode == "per_head" else L)
@@ -154,3 +155,29 @@ def test_in_place_and_scales_refold():
     untouched = (tab == np.arange(tab.size)) & (st.refcount[0].cpu().numpy() == 1)
     untouched &= st.absorber[0].cpu().numpy() == O.NONE
     assert np.array_equal(view.keys.reshape(B * p, -1)[untouched], Kh[0].reshape(B * p, -1)[untouched])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
+@pytest.mark.parametrize("head_mode", ["folded", "per_head"])
+def test_large_groups_vs_oracle(dtype, head_mode):
+    """One tight cluster: every right block of a level-1 merge is absorbed by the same
+    left block (64 members per absorber, past the 32-lane member prefetch of the merge
+    kernels); d = 128 so per-head vectors are 4 KB (the ring merge kernel) and folded
+    vectors 8 KB (the TMA ring merge kernel)."""
+    L, B, p, t, h, d = 1, 4, 64, 16, 2, 128
+    g = torch.Generator(device="cuda").manual_seed(77)
+    base_k = torch.randn((t, h, d), device="cuda", generator=g)
+    base_v = torch.randn((t, h, d), device="cuda", generator=g)
+    Kt = (base_k + 0.05 * torch.randn((L, B, p, t, h, d), device="cuda", generator=g)).to(dtype)
+    Vt = (base_v + 0.05 * torch.randn((L, B, p, t, h, d), device="cuda", generator=g)).to(dtype)
+    Kh, Vh = Kt.double().cpu().numpy(), Vt.double().cpu().numpy()
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8, head_mode=head_mode), keep_samples=True)
+    for oc in outs:
+        st = oc.fused.state
+        ref = O.fuse_unit(O.layer_unit(Kh, oc.report.layer, oc.fused.head),
+                          O.layer_unit(Vh, oc.report.layer, oc.fused.head), B, p, 0.8,
+                          gpu_absorber=st.absorber[oc.fused.unit].cpu().numpy(), eps=EPS[dtype])
+        _compare_unit(oc, ref, dtype)
+        assert max(len(ev.absorbed) for ev in oc.report.fused_events) >= 64
+        assert oc.report.blocks_after == p  # every other row folds into row 0's first block
