@@ -548,6 +548,23 @@ def _head_mode(cfg: FusionConfig) -> int:
 STREAM_LAYERS = 4  # layers per H2D chunk when streaming a host-resident cache
 
 
+def _stream_chunks(L: int) -> list[tuple[int, int]]:
+    """Layer ranges streamed to the GPU: STREAM_LAYERS at a time, the last ones halved
+    (..., 4, 2, 1, 1) so the fusion left after the final copy is one layer's."""
+    out, c0 = [], 0
+    while L - c0 > STREAM_LAYERS:
+        out.append((c0, c0 + STREAM_LAYERS))
+        c0 += STREAM_LAYERS
+    n = L - c0
+    while n > 1:
+        h = (n + 1) // 2
+        out.append((c0, c0 + h))
+        c0, n = c0 + h, n - h
+    if n == 1:
+        out.append((c0, c0 + 1))
+    return out
+
+
 def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_place: bool,
                 keep_samples: bool, path: int) -> list[tuple[FusionState, int]]:
     """Fuse every unit of the cache; returns (state, first layer) per engine run.
@@ -569,7 +586,7 @@ def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_p
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
     copy.wait_stream(compute)  # kd / vd allocated on the compute stream
-    chunks = [(c0, min(d.L, c0 + STREAM_LAYERS)) for c0 in range(0, d.L, STREAM_LAYERS)]
+    chunks = _stream_chunks(d.L)
     ready = []
     with torch.cuda.stream(copy):
         for c0, c1 in chunks:
