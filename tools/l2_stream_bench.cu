@@ -98,6 +98,51 @@ __global__ void k_tma1(const __grid_constant__ CUtensorMap map, int nblocks, int
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// (c) hybrid: each warp streams one 4 KB slot per iteration through a 2-stage TMA ring AND
+// one 4 KB slot by 16-B ld.global (the decode's K by TMA, V by the LSU path)
+template <int W, int NS>
+__global__ void k_hybrid(const __grid_constant__ CUtensorMap map, const uint8_t* __restrict__ pool,
+                         int nblocks, int iters, unsigned* sink) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* st = sm + warp * NS * 4096;
+  uint64_t* bars = (uint64_t*)(sm + W * NS * 4096) + warp * NS;
+  if (lane == 0) for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+  __syncwarp();
+  unsigned acc = 0;
+  const uint32_t seed = blockIdx.x * W + warp;
+  auto issue = [&](int it) {
+    const int s = it % NS;
+    const uint32_t hsh = hash(seed * 7919u + it);
+    const int row = hsh % nblocks, head = (hsh >> 20) & 7;
+    if (lane == 0) {
+      mbar_expect_tx(&bars[s], 4096);
+      tma4(st + s * 4096, &map, &bars[s], 0, head, 0, row);
+      tma4(st + s * 4096 + 2048, &map, &bars[s], 64, head, 0, row);
+    }
+  };
+  for (int i = 0; i < NS - 1 && i < iters; ++i) issue(i);
+  for (int it = 0; it < iters; ++it) {
+    if (it + NS - 1 < iters) issue(it + NS - 1);
+    const uint32_t h2 = hash(seed * 104729u + it);
+    const uint8_t* base = pool + (size_t)(h2 % nblocks) * BLK + ((h2 >> 20) & 7) * D * 2;
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = k * 32 + lane, r = idx >> 4, c = idx & 15;
+      v[k] = __ldg((const uint4*)(base + r * (H * D * 2) + c * 16));
+    }
+    const int s = it % NS;
+    mbar_wait(&bars[s], (it / NS) & 1);
+    acc ^= ((const unsigned*)(st + s * 4096))[lane * 32];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc ^= v[k].x;
+    __syncwarp();
+  }
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+
 // (b) LDG: each warp loads one slot head slice (4 KB = 16 rows x 256 B) per iteration,
 // U slots in flight per warp (unrolled independent loads)
 template <int U>
@@ -187,6 +232,14 @@ int main(int argc, char** argv) {
     run("tma1box W=" #W " NS=" #NS, [&] { k_tma1<W, NS><<<148, W * 32, smem>>>(m2, nblocks, iters, sink); }, \
         148.0 * W * iters * 4096);                                                                      \
   }
+#define HYB(W, NS)                                                                                      \
+  {                                                                                                     \
+    const int smem = 1024 + W * NS * 4096 + W * NS * 8;                                                 \
+    cudaFuncSetAttribute(k_hybrid<W, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);           \
+    run("hybrid tma+ldg W=" #W " NS=" #NS, [&] { k_hybrid<W, NS><<<148, W * 32, smem>>>(m, pool, nblocks, iters, sink); }, \
+        148.0 * W * iters * 8192);                                                                      \
+  }
+  HYB(12, 2) HYB(12, 3) HYB(16, 2) HYB(8, 3)
   TMA1(12, 2) TMA1(12, 3) TMA1(20, 2) TMA1(12, 4) TMA1(24, 2) TMA1(16, 3)
   TMAX(12, 2, 32768) TMAX(12, 2, 65536) TMAX(12, 2, 98304) TMAX(12, 2, 120000)
   TMA(6, 2) TMA(8, 2) TMA(12, 2) TMA(16, 2) TMA(20, 2) TMA(24, 1) TMA(8, 3) TMA(12, 3) TMA(6, 4) TMA(12, 4) TMA(24, 2)
