@@ -518,7 +518,7 @@ def ours_main(args):
                                if graph is None else
                                f"CUDA events around each similarity launch of {len(sim_recs)} eager steps "
                                "run after the timed graph replays (replays carry no per-kernel events)"),
-                "share_of_step": sim_ms / (sum(a.elapsed_time(b) for a, b, _ in sim_recs) * len(recs) / len(sim_recs)),
+                "share_of_step": sim_ms / sum(step_ms),  # of the timed steps (graph replays or eager)
             },
             "gpu_launches": launches,
             "clocks": clk,
