@@ -181,3 +181,30 @@ def test_large_groups_vs_oracle(dtype, head_mode):
         _compare_unit(oc, ref, dtype)
         assert max(len(ev.absorbed) for ev in oc.report.fused_events) >= 64
         assert oc.report.blocks_after == p  # every other row folds into row 0's first block
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVF_RANDOM_CASES", "8"))))
+def test_random_shapes_vs_oracle(seed):
+    """Seeded random geometries (batch, blocks per request, heads, head dim, threshold,
+    dtype, head mode, group size) against the float64 oracle."""
+    rng = np.random.default_rng(1000 + seed)
+    B = int(rng.integers(2, 17))
+    p = int(rng.choice([3, 8, 13, 32, 96]))  # 96: merges span several 256-block tiles
+    h = int(rng.choice([1, 2, 4]))
+    d = int(rng.choice([64, 128]))
+    t = 16
+    thr = float(rng.choice([0.6, 0.75, 0.85]))
+    dtype = [torch.float32, torch.bfloat16][seed % 2]
+    head_mode = ["folded", "per_head"][(seed // 2) % 2]
+    group_size = [None, 2, 3][seed % 3]
+    L = 1
+    cache, Kh, Vh = _cache(L, B, p, t, h, d, dtype, seed=50 + seed)
+    outs = K.fuse_batch(cache, K.FusionConfig(threshold=thr, head_mode=head_mode, group_size=group_size),
+                        keep_samples=True)
+    for oc in outs:
+        st = oc.fused.state
+        ref = O.fuse_unit(O.layer_unit(Kh, oc.report.layer, oc.fused.head),
+                          O.layer_unit(Vh, oc.report.layer, oc.fused.head), B, p, thr,
+                          O.bff_groups(B, group_size),
+                          gpu_absorber=st.absorber[oc.fused.unit].cpu().numpy(), eps=EPS[dtype])
+        _compare_unit(oc, ref, dtype)
