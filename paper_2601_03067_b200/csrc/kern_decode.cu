@@ -384,8 +384,72 @@ static cudaError_t decode_fast_t(const DecodeArgs& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// Split combine without probabilities: one warp per (request, query head). Lane s
+// holds split s's (m, l) (32 splits per pass), the split weights exp(m_s - M) are
+// computed once and broadcast, and each lane accumulates 4 output elements from
+// coalesced 128-B rows of the partials (the CTA-per-head kernel above re-reads
+// every (m, l) in every thread and recomputes the weights per element).
+template <int D>
+__global__ void __launch_bounds__(256)
+decode_combine_warp_kernel(const float* __restrict__ part, int64_t nsplit, int64_t p_blocks,
+                           const int32_t* __restrict__ seq_blocks, int Hq, int64_t n_bh,
+                           float* __restrict__ out, float* __restrict__ lse, int cbs) {
+  constexpr int EPL = D / 32;  // output elements per lane
+  const int lane = threadIdx.x & 31;
+  const int64_t bh = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (bh >= n_bh) return;
+  const float* pp = part + bh * nsplit * (D + 2);
+  const int64_t b = bh / Hq;
+  const int64_t nblk = seq_blocks ? (int64_t)seq_blocks[b] : p_blocks;
+  const int64_t nused = (nblk + cbs - 1) / cbs;
+  float M = -INFINITY;
+  for (int64_t s0 = 0; s0 < nused; s0 += 32)
+    if (s0 + lane < nused) M = fmaxf(M, pp[(s0 + lane) * (D + 2) + D]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float L = 0.f, acc[EPL];
+#pragma unroll
+  for (int k = 0; k < EPL; ++k) acc[k] = 0.f;
+  for (int64_t s0 = 0; s0 < nused; s0 += 32) {
+    float w = 0.f;
+    if (s0 + lane < nused) {
+      const float* ps = pp + (s0 + lane) * (D + 2);
+      const float m = ps[D];
+      w = m == -INFINITY ? 0.f : expf(m - M);
+      L += ps[D + 1] * w;
+    }
+    const int ns = nused - s0 < 32 ? (int)(nused - s0) : 32;
+#pragma unroll 4
+    for (int j = 0; j < ns; ++j) {
+      const float wj = __shfl_sync(0xffffffffu, w, j);
+      const float* ps = pp + (s0 + j) * (D + 2);
+#pragma unroll
+      for (int k = 0; k < EPL; ++k) acc[k] = fmaf(ps[k * 32 + lane], wj, acc[k]);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  const float inv = 1.f / L;
+#pragma unroll
+  for (int k = 0; k < EPL; ++k) out[bh * D + k * 32 + lane] = acc[k] * inv;
+  if (lane == 0) lse[bh] = M + logf(L);
+}
+
 cudaError_t launch_decode_combine(const DecodeArgs& a, int64_t nsplit, int cbs, cudaStream_t s) {
-  decode_combine_kernel<float><<<(unsigned)(a.B * a.Hq), 128, 0, s>>>(
+  const int64_t n_bh = a.B * a.Hq;
+  if (a.g.d == 128 || a.g.d == 64) {
+    const unsigned grid = (unsigned)((n_bh * 32 + 255) / 256);
+    if (a.g.d == 128)
+      decode_combine_warp_kernel<128><<<grid, 256, 0, s>>>((const float*)a.ws, nsplit, a.p_blocks,
+                                                           a.seq_blocks, a.Hq, n_bh, (float*)a.out,
+                                                           (float*)a.lse, cbs);
+    else
+      decode_combine_warp_kernel<64><<<grid, 256, 0, s>>>((const float*)a.ws, nsplit, a.p_blocks,
+                                                          a.seq_blocks, a.Hq, n_bh, (float*)a.out,
+                                                          (float*)a.lse, cbs);
+    return cudaGetLastError();
+  }
+  decode_combine_kernel<float><<<(unsigned)n_bh, 128, 0, s>>>(
       (const float*)a.ws, nsplit, a.g.d, a.p_blocks, a.g.t, a.seq_blocks, a.Hq, (float*)a.out,
       (float*)a.lse, nullptr, cbs);
   return cudaGetLastError();
