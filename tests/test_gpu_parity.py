@@ -208,3 +208,42 @@ def test_random_shapes_vs_oracle(seed):
                           O.bff_groups(B, group_size),
                           gpu_absorber=st.absorber[oc.fused.unit].cpu().numpy(), eps=EPS[dtype])
         _compare_unit(oc, ref, dtype)
+
+
+@pytest.mark.parametrize("case", ["zero_blocks", "fuse_all", "fuse_none", "single_request", "odd_shapes"])
+@pytest.mark.parametrize("head_mode", ["folded", "per_head"])
+def test_edge_cases_bf16_vs_oracle(case, head_mode):
+    """bf16 / tcgen05 path on the edge cases the reference's own tests cover: zero
+    blocks (norm 0: never fusable, directions stay 0), thresholds that fuse (almost)
+    everything or nothing, a single request (no merges), odd batch / block counts."""
+    L, B, p, t, h, d = 1, 6, 8, 16, 2, 128
+    thr = 0.8
+    if case == "single_request":
+        B = 1
+    if case == "odd_shapes":
+        B, p = 5, 7
+    dtype = torch.bfloat16
+    Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=91)
+    if case == "zero_blocks":
+        Kt[0, :, ::3] = 0  # every third block of every request has zero keys
+        Vt[0, 1, 2] = 0    # and one block zero values
+    if case == "fuse_all":
+        thr = -0.95
+    if case == "fuse_none":
+        thr = 0.999
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    Kh, Vh = Kt.double().cpu().numpy(), Vt.double().cpu().numpy()
+    outs = K.fuse_batch(cache, K.FusionConfig(threshold=thr, head_mode=head_mode), keep_samples=True)
+    for oc in outs:
+        st = oc.fused.state
+        ref = O.fuse_unit(O.layer_unit(Kh, oc.report.layer, oc.fused.head),
+                          O.layer_unit(Vh, oc.report.layer, oc.fused.head), B, p, thr,
+                          gpu_absorber=st.absorber[oc.fused.unit].cpu().numpy(), eps=EPS[dtype])
+        _compare_unit(oc, ref, dtype)
+        if case in ("single_request", "fuse_none"):
+            assert oc.report.blocks_after == B * p
+        if case == "zero_blocks":  # zero-key blocks are never absorbed nor absorb
+            zero = [(b, j) for b in range(B) for j in range(0, p, 3)]
+            for ev in oc.report.fused_events:
+                assert tuple(ev.absorber) not in zero
+                assert all(tuple(s) not in zero for s in ev.absorbed)
