@@ -1,6 +1,6 @@
 """Per-level profile of a cfg2-shaped fusion run: alive rows, fused counts, similarity time.
 
-usage: python tools/level_profile.py [L] [compact_from]
+usage: python tools/level_profile.py [L] [compact_from] [B] [p]
 """
 import os
 import sys
@@ -16,7 +16,9 @@ from paper_2601_03067_b200.workload import synthetic_kv  # noqa: E402
 L = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 cf = sys.argv[2] if len(sys.argv) > 2 else "auto"
 cf = None if cf == "none" else ("auto" if cf == "auto" else int(cf))
-B, p, t, h, d = 64, 256, 16, 8, 128
+B = int(sys.argv[3]) if len(sys.argv) > 3 else 64
+p = int(sys.argv[4]) if len(sys.argv) > 4 else 256
+t, h, d = 16, 8, 128
 Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=1000)
 geom = Geometry(L, B * p, t, h, d, 0)
 plan = bff_plan(B, p, None)
