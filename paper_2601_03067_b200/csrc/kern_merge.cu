@@ -798,7 +798,13 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
   const int slot_bytes = (int)((vbytes + 127) / 128 * 128);
   const char* ev = getenv("KVF_MERGE_CTAS_PER_SM");
   const int per_sm = ev ? std::max(1, atoi(ev)) : 2;
-  const int nbuf = (int)std::min<int64_t>(MG_MAX_BUF, (200 * 1024 / per_sm) / slot_bytes);
+  // ring slots per CTA: ~128 KB of copies in flight per SM (more outstanding TMA bytes
+  // per SM lower the delivered rate; cfg2 merges: 3 x 32 KB slots x 2 CTAs 18.1 ms,
+  // 2 x 32 KB x 2 CTAs 17.5 ms per 2 steps); KVF_MERGE_NBUF overrides (measurements)
+  const char* eb = getenv("KVF_MERGE_NBUF");
+  const int64_t fit = std::min<int64_t>(MG_MAX_BUF, (200 * 1024 / per_sm) / slot_bytes);  // smem
+  const int nbuf = (int)std::min<int64_t>(
+      fit, eb ? std::max(2, atoi(eb)) : std::max<int64_t>(2, (128 * 1024 / per_sm) / slot_bytes));
   const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
