@@ -809,17 +809,13 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    // per-head units of 4 KB: warp per item, per-warp smem ring (3 slots)
-    if (g.head_mode && vbytes == 4096 && g.t <= 32 && (g.d * 2) % 16 == 0 && can_vectorize<T>(pk, g) &&
-        can_vectorize<T>(pv, g) && !getenv("KVF_MERGE_NO_RING")) {
+    // per-head units of 2 or 4 KB: warp per item, per-warp smem ring (3 slots)
+    if (g.head_mode && (vbytes == 4096 || vbytes == 2048) && g.t <= 32 && (g.d * 2) % 16 == 0 &&
+        can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g) && !getenv("KVF_MERGE_NO_RING")) {
       auto go = [&](auto kern, int ns, int wpb, int per_sm) {
-        const int smem = wpb * ns * 4096 + wpb * ns * (8 + (int)sizeof(RingSlotMeta));
-        static bool attr = false;
-        if (!attr) {
-          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-          if (e != cudaSuccess) return e;
-          attr = true;
-        }
+        const int smem = wpb * ns * (int)vbytes + wpb * ns * (8 + (int)sizeof(RingSlotMeta));
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
         kern<<<148 * per_sm, wpb * 32, smem, s>>>((__nv_bfloat16*)pk, (__nv_bfloat16*)pv, g, (float*)kn,
                                                   (float*)vn, (const float*)okn, (const float*)ovn, ws,
                                                   n_total);
@@ -827,7 +823,7 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
       };
       // measured (cfg2 per-head, 2 steps): 8 warps x 3 slots x 2 CTAs/SM 23.6 ms; 6 x 4 x 2 28.6;
       // 4 x 5 x 3 51.2; 8 x 3 x 1 41.1 (merge_warp_kernel: 28.2)
-      return go(merge_ring_kernel<8, 3>, 3, 8, 2);
+      return vbytes == 4096 ? go(merge_ring_kernel<8, 3>, 3, 8, 2) : go(merge_ring_kernel<4, 3>, 3, 8, 2);
     }
   }
   if constexpr (!std::is_same<T, double>::value) {
