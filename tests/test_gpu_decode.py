@@ -191,3 +191,31 @@ def test_scheduled_decode_block_sizes(t, d):
         got, _ = K.paged_decode(q, st, 0, B, p, schedule=sched)
         want = _reference(q, st, 0, B, p, sb)
         torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVF_RANDOM_CASES", "6"))))
+def test_random_decode_vs_reference(seed):
+    """Seeded random shapes through both decode paths (request-major and sharing-aware,
+    with and without ragged lengths) against the float64 refold + softmax reference."""
+    rng = np.random.default_rng(500 + seed)
+    B = int(rng.integers(1, 10))
+    p = int(rng.integers(1, 70))
+    h = int(rng.choice([1, 2, 4, 8]))
+    G = int(rng.choice([1, 2, 4, 8]))
+    d = int(rng.choice([64, 128]))
+    t = 16
+    head_mode = ["folded", "per_head"][seed % 2]
+    Kt, Vt = synthetic_kv(1, B, p, t, h, d, dtype=torch.bfloat16, seed=600 + seed)
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=1), Kt, Vt)
+    st = K.fuse_batch(cache, K.FusionConfig(threshold=float(rng.choice([0.7, 0.8])), head_mode=head_mode),
+                      keep_samples=False)[0].fused.state
+    q = torch.randn((B, h * G, d), device="cuda", dtype=torch.bfloat16,
+                    generator=torch.Generator(device="cuda").manual_seed(seed))
+    seq = torch.tensor(rng.integers(1, p + 1, size=B), dtype=torch.int32, device="cuda")
+    for sb in (None, seq):
+        want = _reference(q, st, 0, B, p, sb)
+        got, _ = K.paged_decode(q, st, 0, B, p, seq_blocks=sb)
+        torch.testing.assert_close(got.double(), want, atol=2e-3, rtol=2e-3)
+        sched = K.state_decode_schedule(st, 0, B, p, seq_blocks=sb)
+        got2, _ = K.paged_decode(q, st, 0, B, p, schedule=sched)
+        torch.testing.assert_close(got2.double(), want, atol=2e-3, rtol=2e-3)
