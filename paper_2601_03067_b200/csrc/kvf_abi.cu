@@ -421,7 +421,10 @@ int kvf_chunk_prefill(const void* q, const void* pool_k, const void* pool_v, int
   // path: 0 auto (tcgen05 when the shape allows: 3.7 vs 9.7 ms mma.sync on the last
   // chunk of 4 x 16K), 1 mma.sync, 2 tcgen05
   const bool tc_ok = chunk_prefill_tc_supported(a);
-  if (path == 2 && !tc_ok) return fail(KVF_ERR_INVALID, "tcgen05 chunked prefill needs d = 128, t = 16");
+  if (path == 2 && !tc_ok)
+    return fail(KVF_ERR_INVALID,
+                "tcgen05 chunked prefill needs d = 128, t = 16, folded units, 128 %% G == 0, "
+                "chunk tokens a multiple of 256 / G and p <= 1024 (path = auto falls back to mma.sync)");
   if (path != 1 && tc_ok)
     return cuda_status(launch_chunk_prefill_tc(a, (cudaStream_t)stream), "kvf_chunk_prefill[tc]");
   return cuda_status(launch_chunk_prefill(a, (cudaStream_t)stream), "kvf_chunk_prefill");

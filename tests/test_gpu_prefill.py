@@ -59,3 +59,30 @@ def test_chunk_prefill_vs_reference(G, d, path):
         torch.testing.assert_close(got.double(), want, atol=3e-3, rtol=3e-3)
         slot = K.chunk_prefill(q, st, 0, B, p, chunk_blocks, chunk, dedup=False, path=path)
         torch.testing.assert_close(got, slot, atol=2e-3, rtol=2e-3)
+
+
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("KVF_RANDOM_CASES", "4"))))
+def test_random_chunk_prefill_vs_reference(seed):
+    """Seeded random CFF geometries (batch, chunk size, GQA group, kernel path) for
+    chunked prefill with and without per-block reuse."""
+    import numpy as np
+
+    rng = np.random.default_rng(900 + seed)
+    t, h, d = 16, 2, 128
+    B = int(rng.integers(1, 4))
+    chunk_blocks = int(rng.choice([8, 16]))
+    C = int(rng.choice([2, 4]))
+    p = chunk_blocks * C
+    G = int(rng.choice([1, 2, 4, 8]))
+    path = ["auto", "mma"][seed % 2]  # auto: tcgen05 where the shape allows
+    Kt, Vt = synthetic_kv(1, B, p, t, h, d, dtype=torch.bfloat16, seed=950 + seed, variant="cff")
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=1), Kt, Vt)
+    st = K.fuse_chunks(cache, K.FusionConfig(threshold=0.8, variant="cff"), chunk_blocks * t,
+                       keep_samples=False)[0].fused.state
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    for chunk in range(C):
+        q = torch.randn((B, chunk_blocks * t, h * G, d), device="cuda", dtype=torch.bfloat16, generator=g)
+        want = _reference(q, st, 0, B, p, chunk_blocks, chunk)
+        for dedup in (True, False):
+            got = K.chunk_prefill(q, st, 0, B, p, chunk_blocks, chunk, dedup=dedup, path=path)
+            torch.testing.assert_close(got.double(), want, atol=3e-3, rtol=3e-3)
