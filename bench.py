@@ -716,10 +716,25 @@ def bench_e2e(args, c, K0, V0, dtype, dev, world, torch, dist, PagedKvCache, Cac
               fuse_batch, fuse_chunks):
     """Same metric through the public API (PagedKvCache + fuse_batch) from pinned host buffers;
     every step copies the cache H2D and reads tables / refcounts / scales back D2H."""
-    Kh = torch.empty(K0.shape, dtype=dtype, pin_memory=True)
-    Vh = torch.empty(V0.shape, dtype=dtype, pin_memory=True)
-    Kh.copy_(K0)
-    Vh.copy_(V0)
+    ok, why = 1, ""
+    try:  # pinned host copies of the cache (N ranks pin N x the cache bytes on the host)
+        Kh = torch.empty(K0.shape, dtype=dtype, pin_memory=True)
+        Vh = torch.empty(V0.shape, dtype=dtype, pin_memory=True)
+        Kh.copy_(K0)
+        Vh.copy_(V0)
+    except Exception as exc:  # every rank agrees before any other collective
+        ok, why = 0, f"pinned host buffers: {str(exc)[:160]}"
+    if world > 1:
+        flag = torch.tensor([ok], dtype=torch.int64, device=dev)
+        if dist_backend() == "nccl":
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        else:
+            h = flag.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MIN)
+            flag.copy_(h)
+        ok = int(flag.item())
+    if not ok:
+        return {"value": None, "unit": "GB/s", "error": why or "a peer rank could not pin its host buffers"}
     dims = CacheDims(B=c["B"], p=c["p"], t=c["t"], h=c["h"], d=c["d"], L=c["L"])
     cfg = FusionConfig(threshold=c["thr"], variant=c["variant"], head_mode=args.head_mode)
 
