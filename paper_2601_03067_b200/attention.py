@@ -96,8 +96,8 @@ class DecodeSchedule:
 
     order[hu, b, :] lists request b's block positions sorted by the physical
     block they map to (-1 past seq_blocks); the n_items[hu] items -- chunks of
-    `item_blocks` sorted positions of one request -- are ordered by their first
-    physical block: meta[hu, i] = b * nit + k, and phys / ks / vs[hu, i, :]
+    `item_blocks` sorted positions of one request -- are ordered by the physical
+    block of their middle slot: meta[hu, i] = b * nit + k, and phys / ks / vs[hu, i, :]
     hold the item's physical blocks (-1 = padding) and K / V scales. Softmax
     is permutation invariant, so decoding in this order gives the
     request-major result (up to fp32 summation order) while requests sharing

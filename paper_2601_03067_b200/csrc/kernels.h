@@ -157,7 +157,7 @@ cudaError_t launch_decode_tma(const DecodeArgs& a, cudaStream_t s);
 // sharing-aware decode (kern_decode_sched.cu). A schedule lists, per head
 // unit hu (h units in per_head mode, else 1), `n_items` items of `ib` slots:
 //   meta[hu][i]          = b * nit + k  (request b, k-th item of b), items in
-//                          ascending order of their first physical block
+//                          ascending order of their middle slot's physical block
 //   phys/ks/vs[hu][i][j] = physical block / K scale / V scale of the item's
 //                          j-th slot (slots of a request in ascending phys
 //                          order); phys = -1 marks padding past seq_blocks

@@ -104,8 +104,10 @@ def test_scheduled_decode_vs_reference(d, G, head_mode, ib):
                 tab, ksc, vsc = st.table[u].cpu(), st.k_scale[u].cpu(), st.v_scale[u].cpu()
                 meta = sched.meta[hu, :n_valid].cpu().long()
                 phys = sched.phys[hu, :n_valid].cpu()
-                firsts = phys[:, 0].tolist()
-                assert firsts == sorted(firsts)  # items swept by first physical block
+                # items swept by the physical block of their middle slot
+                nvalid = (phys >= 0).sum(1)
+                keys = [int(phys[i, (int(nvalid[i]) - 1) // 2]) for i in range(len(phys))]
+                assert keys == sorted(keys)
                 assert sorted(meta.tolist()) == sorted(
                     b * nit + k for b in range(B) for k in range((int(nblk[b]) + ib - 1) // ib))
                 for row, it in enumerate(meta.tolist()):
