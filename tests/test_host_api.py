@@ -150,3 +150,19 @@ def test_percentile_adaptation_on_device_samples():
     host = adapt_threshold(pol, FusionReport.aggregate(reports), 0.5)
     want = float(np.quantile(np.concatenate([r.similarity_samples for r in reports]), 0.8))
     assert dev == host == want
+
+
+def test_stream_chunks_cover_layers_in_order():
+    """Host-resident streaming: layer chunks cover [0, L) in order, full STREAM_LAYERS
+    chunks first, then halving so one layer's fusion is left after the last copy."""
+    from paper_2601_03067_b200.fusion import STREAM_LAYERS, _stream_chunks
+
+    for L in range(1, 70):
+        ch = _stream_chunks(L)
+        assert ch[0][0] == 0 and ch[-1][1] == L
+        assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+        sizes = [c1 - c0 for c0, c1 in ch]
+        assert all(0 < s <= STREAM_LAYERS for s in sizes)
+        assert sizes == sorted(sizes, reverse=True)
+        if L > 1:
+            assert sizes[-1] == 1
