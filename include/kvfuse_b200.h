@@ -90,7 +90,11 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
  * units) they are gathered straight from the pool with TMA gather4.
  * Re-score (tcgen05 path): pairs with |sim - thr| <= rescore_band are queued
  * (int32[4 * (rescore_cap + 1)], entries then the count) and decided from a
- * float64 recomputation in the same call; NULL / 0 disables it. */
+ * float64 recomputation in the same call; NULL / 0 disables it.
+ * filter (float32 pools): bf16 copy of the pool (kvf_convert_rows) that the
+ *   tensor cores read; the re-score reads the float32 pool.
+ * shadow / sidx (exact mode, kvf_exact_merge_keys): the re-score reads a fused
+ *   key from its fp32 shadow row instead of the rounded pool block. */
 int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           int t, int h, int d, int head_mode, int64_t u0,
                           int64_t nU, const void* knorm, const uint8_t* fusable,
@@ -100,8 +104,30 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           const int64_t* sample_off, int64_t sample_stride,
                           const int32_t* live, const int32_t* rank,
                           const void* staged, int32_t* rescore_queue,
-                          int64_t rescore_cap, double rescore_band, int path,
-                          void* stream);
+                          int64_t rescore_cap, double rescore_band,
+                          const void* filter, const float* shadow,
+                          const int32_t* sidx, int path, void* stream);
+
+/* Exact-decision key merge (bf16 pools; replaces the K half of
+ * kvf_merge_groups, fusion.py:259-261 / _unit 285-287 in float64): for each
+ * absorber of the level, dir = unit(sum of the members' float64 directions)
+ * -- shadow[sidx[j]] for members fused earlier, x_j / |x_j| (float64) of the
+ * original block otherwise; dir is kept as an fp32 shadow row (slot taken
+ * from *shadow_count on first fusion, up to shadow_cap; overflowing absorbers
+ * keep sidx = -1 and the count exceeds the cap) and written to the pool as
+ * bf16(s_home * dir) with its stored norm. r <= 16384. */
+int kvf_exact_merge_keys(void* pool_k, int dtype, int64_t L, int64_t NB,
+                         int t, int h, int d, int head_mode, float* knorm,
+                         const float* orig_knorm, float* shadow,
+                         int64_t shadow_cap, int32_t* sidx,
+                         int32_t* shadow_count, int32_t* level_ws,
+                         void* stream);
+
+/* bf16 operand copy of a float32 pool for the tcgen05 similarity: every
+ * vector (level_ws == NULL) or the key absorbers of the current level. */
+int kvf_convert_rows(const void* src, int src_dtype, void* dst, int64_t L,
+                     int64_t NB, int t, int h, int d, int head_mode,
+                     int32_t* level_ws, void* stream);
 
 /* Ascending alive list live[U][NB], exclusive rank[U][NB + 1] (number of
  * alive blocks before each id) and count[U] for units [u0, u0 + nU). */
@@ -135,11 +161,13 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB,
  * for each absorber l, dir = unit(dir_l + sum_{j: absorber[j]=l} dir_j) for K
  * and the same indices for V (members summed in ascending order); written
  * back as s_home * dir with s_home the home slot's original norm (1 if
- * zero); stored norm recomputed from the rounded values. */
+ * zero); stored norm recomputed from the rounded values. which: 1 = K only,
+ * 2 = V only, 3 = both (the exact-decision mode merges K with
+ * kvf_exact_merge_keys). */
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L,
                      int64_t NB, int t, int h, int d, int head_mode, void* knorm,
                      void* vnorm, const void* orig_knorm, const void* orig_vnorm,
-                     int32_t* level_ws, void* stream);
+                     int32_t* level_ws, int which, void* stream);
 
 /* K5 -- block-table remap + refcounts (replaces BlockTable.redirect,
  * core.py:217-227, and alive[rid] = False, fusion.py:262-264); resets the

@@ -48,8 +48,13 @@ SIGNATURES: dict[str, tuple] = {
         _i32,
         [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp,
          _vp, _i32, _vp, _i32, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _f64,
-         _i32, _vp],
+         _vp, _vp, _vp, _i32, _vp],
     ),
+    "kvf_exact_merge_keys": (
+        _i32,
+        [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    ),
+    "kvf_convert_rows": (_i32, [_vp, _i32, _vp, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),
     "kvf_alive_rank": (_i32, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "kvf_stage_rows": (
         _i32, [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp]
@@ -60,7 +65,8 @@ SIGNATURES: dict[str, tuple] = {
         [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp, _vp],
     ),
     "kvf_merge_groups": (
-        _i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp]
+        _i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32,
+               _vp]
     ),
     "kvf_remap": (_i32, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kvf_finalize": (

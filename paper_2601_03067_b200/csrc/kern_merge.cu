@@ -191,6 +191,16 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_tot
   return cudaGetLastError();
 }
 
+// Item selection of the merge kernels: which = 3 merges K and V (items 2a, 2a+1
+// = K, V of absorber a), 1 = K only, 2 = V only (the exact-decision mode merges
+// the keys separately, kern_exact.cu)
+struct ItemSel {
+  int which;
+  __device__ __forceinline__ int64_t n(int64_t count) const { return which == 3 ? 2 * count : count; }
+  __device__ __forceinline__ bool is_v(int64_t it) const { return which == 3 ? (it & 1) : which == 2; }
+  __device__ __forceinline__ int64_t idx(int64_t it) const { return which == 3 ? (it >> 1) : it; }
+};
+
 // ---------------------------------------------------------------------------
 // K4 main path: bulk-copy ring + register accumulation
 // ---------------------------------------------------------------------------
@@ -255,7 +265,7 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
 merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* __restrict__ knorm,
                  float* __restrict__ vnorm, const float* __restrict__ oknorm,
                  const float* __restrict__ ovnorm, int32_t* ws, int64_t n_total, int nbuf,
-                 int slot_bytes) {
+                 int slot_bytes, ItemSel sel) {
   constexpr int VEC = 16 / (int)sizeof(T);
   constexpr int CPT = EPT / VEC;  // 16-byte chunks per consumer thread
   extern __shared__ __align__(128) uint8_t msm[];
@@ -268,7 +278,7 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = g.r();
   const uint32_t vbytes = (uint32_t)(r * (int64_t)sizeof(T));
-  const int n_items = 2 * (*W.count);
+  const int n_items = (int)sel.n(*W.count);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < nbuf; ++s) {
@@ -296,9 +306,9 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       x.inv = 0.f;
       x.home = 0.f;
       if (!x.valid) return x;
-      const bool is_v = it & 1;
+      const bool is_v = sel.is_v(it);
       const float* norm = is_v ? vnorm : knorm;
-      x.gid = W.list[it >> 1];
+      x.gid = W.list[sel.idx(it)];
       x.n = W.mcnt[x.gid];
       const int64_t gb = (x.gid / g.NB) * g.NB;
       const int s0 = W.mstart[x.gid];
@@ -315,7 +325,7 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
     Item cur = load_item(it);
     while (cur.valid) {
       const Item nxt = load_item(it + gridDim.x);
-      const bool is_v = it & 1;
+      const bool is_v = sel.is_v(it);
       const T* pool = is_v ? pool_v : pool_k;
       const int64_t u = cur.gid / g.NB;
       const int64_t gb = u * g.NB;
@@ -428,13 +438,13 @@ merge_reg_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
                  typename AccOf<T>::type* __restrict__ vnorm,
                  const typename AccOf<T>::type* __restrict__ oknorm,
                  const typename AccOf<T>::type* __restrict__ ovnorm, int32_t* ws,
-                 int64_t n_total) {
+                 int64_t n_total, ItemSel sel) {
   using A = typename AccOf<T>::type;
   constexpr int MAXQ = 32 / VEC;
   __shared__ A red[32];
   const LevelWs W(ws, n_total);
   const int tid = threadIdx.x, bd = blockDim.x;
-  const bool is_v = blockIdx.y == 1;
+  const bool is_v = sel.which == 3 ? blockIdx.y == 1 : sel.which == 2;
   T* pool = is_v ? pool_v : pool_k;
   A* norm = is_v ? vnorm : knorm;
   const A* onorm = is_v ? ovnorm : oknorm;
@@ -506,17 +516,17 @@ __global__ void __launch_bounds__(256, 2)
 merge_warp_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
                   float* __restrict__ knorm, float* __restrict__ vnorm,
                   const float* __restrict__ oknorm, const float* __restrict__ ovnorm,
-                  int32_t* ws, int64_t n_total) {
+                  int32_t* ws, int64_t n_total, ItemSel sel) {
   const LevelWs W(ws, n_total);
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_items = 2 * (int64_t)(*W.count);
+  const int64_t n_items = sel.n(*W.count);
   for (int64_t it = warp; it < n_items; it += nwarps) {
-    const bool is_v = it & 1;
+    const bool is_v = sel.is_v(it);
     T* pool = is_v ? pool_v : pool_k;
     float* norm = is_v ? vnorm : knorm;
-    const int64_t gid = W.list[it >> 1];
+    const int64_t gid = W.list[sel.idx(it)];
     const int64_t u = gid / g.NB;
     const int64_t gb = u * g.NB;
     const int32_t l = (int32_t)(gid % g.NB);
@@ -601,7 +611,7 @@ __global__ void __launch_bounds__(256, 2)
 merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict__ pool_v, Geom g,
                   float* __restrict__ knorm, float* __restrict__ vnorm,
                   const float* __restrict__ oknorm, const float* __restrict__ ovnorm,
-                  int32_t* ws, int64_t n_total) {
+                  int32_t* ws, int64_t n_total, ItemSel sel) {
   constexpr int VB = CPL * 512;  // vector bytes (32 lanes x CPL x 16 B)
   extern __shared__ __align__(128) uint8_t rsm[];
   const LevelWs W(ws, n_total);
@@ -616,7 +626,7 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
   __syncwarp();
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t n_items = 2 * (int64_t)(*W.count);
+  const int64_t n_items = sel.n(*W.count);
   const uint32_t segb = (uint32_t)(g.d * 2);
   const int64_t rstride = (int64_t)g.h * g.d;  // elements between token rows
 
@@ -628,9 +638,9 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
   float inv_l = 0.f, home_i = 0.f;
   auto load_item = [&]() {  // all lanes
     if (it_i >= n_items) return;
-    const bool is_v = it_i & 1;
+    const bool is_v = sel.is_v(it_i);
     const float* norm = is_v ? vnorm : knorm;
-    gid_i = W.list[it_i >> 1];
+    gid_i = W.list[sel.idx(it_i)];
     n_i = W.mcnt[gid_i];
     s0_i = W.mstart[gid_i];
     home_i = (is_v ? ovnorm : oknorm)[gid_i];
@@ -646,7 +656,7 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
   uint32_t q_i = 0, q_c = 0;
   auto issue = [&]() {  // all lanes
     if (it_i >= n_items) return;
-    const bool is_v = it_i & 1;
+    const bool is_v = sel.is_v(it_i);
     int32_t id;
     float inv;
     if (v_i < 32) {
@@ -745,21 +755,21 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
 namespace {
 template <typename T, int VEC>
 cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
-                      const void* ovn, int32_t* ws, int64_t n_total, cudaStream_t s) {
+                      const void* ovn, int32_t* ws, int64_t n_total, ItemSel sel, cudaStream_t s) {
   using A = typename AccOf<T>::type;
   const int64_t nch = g.r() / VEC;
   int bd = 512;
   while (bd > 64 && (int64_t)(bd / 2) * (32 / VEC) >= nch) bd /= 2;
   if (nch > (int64_t)bd * (32 / VEC)) return cudaErrorInvalidValue;
-  dim3 grid(148 * 4, 2);
+  dim3 grid(148 * 4, sel.which == 3 ? 2 : 1);
   merge_reg_kernel<T, VEC><<<grid, bd, 0, s>>>((T*)pk, (T*)pv, g, (A*)kn, (A*)vn, (const A*)okn,
-                                               (const A*)ovn, ws, n_total);
+                                               (const A*)ovn, ws, n_total, sel);
   return cudaGetLastError();
 }
 
 template <typename T, int EPT>
 cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
-                      const void* ovn, int32_t* ws, int64_t n_total, int nbuf, int slot_bytes,
+                      const void* ovn, int32_t* ws, int64_t n_total, int nbuf, int slot_bytes, ItemSel sel,
                       cudaStream_t s) {
   const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + MG_MAX_BUF * (int)sizeof(SlotMeta) + 64;
   static int attr = 0;  // per instantiation
@@ -785,13 +795,14 @@ cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, con
   }();
   merge_tma_kernel<T, EPT><<<per_sm * n_sm, MG_THREADS, smem, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn,
                                                          (const float*)okn, (const float*)ovn, ws,
-                                                         n_total, nbuf, slot_bytes);
+                                                         n_total, nbuf, slot_bytes, sel);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
-                           const void* ovn, int32_t* ws, int64_t n_total, cudaStream_t s) {
+                           const void* ovn, int32_t* ws, int64_t n_total, ItemSel sel,
+                           cudaStream_t s) {
   constexpr int VEC = Vec16<T>::N;
   const int64_t r = g.r();
   const int64_t vbytes = r * (int64_t)sizeof(T);
@@ -818,7 +829,7 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
         if (e != cudaSuccess) return e;
         kern<<<148 * per_sm, wpb * 32, smem, s>>>((__nv_bfloat16*)pk, (__nv_bfloat16*)pv, g, (float*)kn,
                                                   (float*)vn, (const float*)okn, (const float*)ovn, ws,
-                                                  n_total);
+                                                  n_total, sel);
         return cudaGetLastError();
       };
       // measured (cfg2 per-head, 2 steps): 8 warps x 3 slots x 2 CTAs/SM 23.6 ms; 6 x 4 x 2 28.6;
@@ -833,7 +844,7 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
       const int cpl = (int)(r / (32 * VEC));
       auto launch = [&](auto kern) {
         kern<<<148 * 8, 256, 0, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn, (const float*)okn,
-                                     (const float*)ovn, ws, n_total);
+                                     (const float*)ovn, ws, n_total, sel);
         return cudaGetLastError();
       };
       if (cpl == 1) return launch(merge_warp_kernel<T, VEC, 1>);
@@ -844,34 +855,37 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
     if (tma_ok) {
       const int64_t ept = (r + MG_CONSUMERS - 1) / MG_CONSUMERS;
       if (ept <= 8)
-        return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+        return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
       if (ept <= 16)
-        return merge_tma<T, 16>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+        return merge_tma<T, 16>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
       if (ept <= 32)
-        return merge_tma<T, 32>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
-      return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, s);
+        return merge_tma<T, 32>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
+      return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
     }
   }
   if (can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g))
-    return merge_reg<T, VEC>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, s);
-  return merge_reg<T, 1>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, s);
+    return merge_reg<T, VEC>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, sel, s);
+  return merge_reg<T, 1>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, sel, s);
 }
 }  // namespace
 
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
-                                const void* ovnorm, int32_t* level_ws, cudaStream_t s) {
+                                const void* ovnorm, int32_t* level_ws, int which,
+                                cudaStream_t s) {
+  if (which < 1 || which > 3) return cudaErrorInvalidValue;
+  const ItemSel sel{which};
   const int64_t n_total = g.units() * g.NB;
   switch (dtype) {
     case F64:
       return merge_dispatch<double>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, level_ws,
-                                    n_total, s);
+                                    n_total, sel, s);
     case F32:
       return merge_dispatch<float>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, level_ws,
-                                   n_total, s);
+                                   n_total, sel, s);
     default:
       return merge_dispatch<__nv_bfloat16>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm,
-                                           level_ws, n_total, s);
+                                           level_ws, n_total, sel, s);
   }
 }
 

@@ -5,6 +5,8 @@
 // pair (u, i, j) is recomputed here in float64 from the stored blocks --
 // cos = <x_i, x_j> / sqrt(<x_i, x_i> <x_j, x_j>) -- and, if it exceeds thr,
 // applied with the same order-independent atomicMin as the main epilogue.
+// Exact mode (kern_exact.cu): a block with a shadow slot is read from its
+// float64-derived fp32 unit direction instead of the rounded pool block.
 #include "kernels.h"
 #include "vec_io.cuh"
 
@@ -20,7 +22,8 @@ rescore_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
                const int4* __restrict__ list, const int32_t* __restrict__ count,
                int64_t cap, double thr, int32_t* absorber,
                const int32_t* __restrict__ merges, double* samples,
-               const int64_t* __restrict__ sample_off, int64_t sample_stride) {
+               const int64_t* __restrict__ sample_off, int64_t sample_stride,
+               const float* __restrict__ shadow, const int32_t* __restrict__ sidx) {
   using A = typename AccOf<T>::type;
   __shared__ double red[3][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -31,11 +34,25 @@ rescore_kernel(const T* __restrict__ pool, Geom g, int64_t u0,
     const int64_t u = e.x;
     const T* x = pool + g.base(u, e.y);
     const T* y = pool + g.base(u, e.z);
+    const int32_t sx = sidx ? sidx[u * g.NB + e.y] : -1;
+    const int32_t sy = sidx ? sidx[u * g.NB + e.z] : -1;
+    const float* xs = sx >= 0 ? shadow + (int64_t)sx * g.r() : nullptr;
+    const float* ys = sy >= 0 ? shadow + (int64_t)sy * g.r() : nullptr;
     double dxy = 0.0, dxx = 0.0, dyy = 0.0;
     for (int64_t c = threadIdx.x; c < nch; c += blockDim.x) {
       A a[VEC], b[VEC];
-      VecIO<T, VEC>::load_nc(x + g.off(c * VEC), a);
-      VecIO<T, VEC>::load_nc(y + g.off(c * VEC), b);
+      if (xs) {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) a[q] = (A)xs[c * VEC + q];
+      } else {
+        VecIO<T, VEC>::load_nc(x + g.off(c * VEC), a);
+      }
+      if (ys) {
+#pragma unroll
+        for (int q = 0; q < VEC; ++q) b[q] = (A)ys[c * VEC + q];
+      } else {
+        VecIO<T, VEC>::load_nc(y + g.off(c * VEC), b);
+      }
 #pragma unroll
       for (int q = 0; q < VEC; ++q) {
         const double da = (double)a[q], db = (double)b[q];
@@ -78,11 +95,11 @@ static cudaError_t rescore_t(const RescoreArgs& a, cudaStream_t s) {
   if (can_vectorize<T>(a.pool, a.g))
     rescore_kernel<T, Vec16<T>::N><<<grid, 256, 0, s>>>(
         (const T*)a.pool, a.g, a.u0, (const int4*)a.resc, a.resc_count, a.resc_cap, a.thr,
-        a.absorber, a.merges, a.samples, a.sample_off, a.sample_stride);
+        a.absorber, a.merges, a.samples, a.sample_off, a.sample_stride, a.shadow, a.sidx);
   else
     rescore_kernel<T, 1><<<grid, 256, 0, s>>>(
         (const T*)a.pool, a.g, a.u0, (const int4*)a.resc, a.resc_count, a.resc_cap, a.thr,
-        a.absorber, a.merges, a.samples, a.sample_off, a.sample_stride);
+        a.absorber, a.merges, a.samples, a.sample_off, a.sample_stride, a.shadow, a.sidx);
   return cudaGetLastError();
 }
 

@@ -245,7 +245,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               const int64_t* __restrict__ sample_off, int64_t sample_stride,
               const int32_t* __restrict__ live, const int32_t* __restrict__ rank,
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
-              float resc_band, int32_t* __restrict__ work_counter, int gathered) {
+              float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* meta = smem + STAGES * STAGE_BYTES;
@@ -272,6 +272,11 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   const int layer_div = g.head_mode ? g.h : 1;
   const int dpc = g.d / BK;
   const int nk = g.head_mode ? g.t * dpc : g.t * g.h * dpc;
+  // split3 (float32 pools): the operand copy holds hi = bf16(x) in rows [0, L*NB) and
+  // lo = bf16(x - hi) in rows [L*NB, 2*L*NB); three passes over K accumulate
+  // hi.hi + hi.lo + lo.hi (the dropped lo.lo term is ~2^-16 relative)
+  const int nk_run = split3 ? 3 * nk : nk;
+  const int lo_rows = (int)(g.L * g.NB);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -360,10 +365,12 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int rowB =
           (staged ? (int)(t.ul * g.NB) + t.pm + t.j0 : layer * g.NB + t.mid + t.j0) +
           (int)crank * BNH;
-      for (int ks = 0; ks < nk; ++ks, ++kk) {
+      for (int kr = 0; kr < nk_run; ++kr, ++kk) {
         const int s = kk % STAGES;
         const uint32_t ph = (kk / STAGES) & 1;
         mbar_wait(&empty_bar[s], ph ^ 1);
+        const int part = kr / nk;  // split3 pass: 0 hi.hi, 1 hi.lo, 2 lo.hi
+        const int ks = kr - part * nk;
         const int dc = ks % dpc;
         const int rest = ks / dpc;
         const int hh = g.head_mode ? head : rest % g.h;
@@ -373,8 +380,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         uint8_t* sa = smem + s * STAGE_BYTES;
         uint8_t* sb = sa + A_BYTES;
         if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
-        tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA);
-        tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB);
+        tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA + (part == 2 ? lo_rows : 0));
+        tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB + (part == 1 ? lo_rows : 0));
       }
     }
   } else if (warp == 3) {
@@ -432,7 +439,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         mbar_wait_cluster(&tmem_empty[acc], ((tc >> 1) & 1) ^ 1);  // epilogue drained it
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dst = tmem_base + acc * BN;
-        for (int ks = 0; ks < nk; ++ks, ++kk) {
+        for (int ks = 0; ks < nk_run; ++ks, ++kk) {
           const int s = kk % STAGES;
           const uint32_t ph = (kk / STAGES) & 1;
           mbar_wait(&full_bar[s], ph);
@@ -697,7 +704,7 @@ bool tc_supported(const SimArgs& a, const char** why) {
     *why = "pool pointer must be 16-byte aligned";
     return false;
   }
-  if (a.g.L * a.g.NB >= (int64_t)INT32_MAX - 512) {
+  if (a.g.L * a.g.NB * (a.split3 ? 2 : 1) >= (int64_t)INT32_MAX - 512) {
     *why = "too many pool rows for int32 TMA coordinates";
     return false;
   }
@@ -725,8 +732,10 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   const bool staged = compact && !gathered;
   if (gathered && g.head_mode) return cudaErrorInvalidValue;
   const cuuint64_t r = (cuuint64_t)g.r();
+  const bool split3 = a.split3 != 0;
+  if (split3 && compact) return cudaErrorInvalidValue;
   cuuint64_t dims[4] = {(cuuint64_t)g.d, (cuuint64_t)g.h, (cuuint64_t)g.t,
-                        (cuuint64_t)(g.L * g.NB)};
+                        (cuuint64_t)(g.L * g.NB * (split3 ? 2 : 1))};
   cuuint64_t strides[3] = {(cuuint64_t)g.d * 2, (cuuint64_t)g.h * g.d * 2,
                            (cuuint64_t)g.t * g.h * g.d * 2};
   if (staged) {  // staged rows: [nU * NB][r] -> (64, r/64, 1, rows)
@@ -788,7 +797,7 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
       tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
-      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? 1 : 0);
+      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? 1 : 0, split3 ? 1 : 0);
   return cudaGetLastError();
 }
 

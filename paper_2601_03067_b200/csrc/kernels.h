@@ -43,6 +43,8 @@ struct SimArgs {
   int32_t* resc_count = nullptr;
   int64_t resc_cap = 0;
   double resc_band = 0.0;
+  // float32 pools: `pool` is the hi/lo bf16 split copy (2 * L * NB rows, kvf_convert_rows)
+  int split3 = 0;
 };
 
 struct RescoreArgs {
@@ -59,6 +61,8 @@ struct RescoreArgs {
   double* samples;
   const int64_t* sample_off;
   int64_t sample_stride;
+  const float* shadow = nullptr;  // exact mode: fp32 unit directions of fused keys
+  const int32_t* sidx = nullptr;  // [U][NB] shadow slot or -1
 };
 cudaError_t launch_rescore(const RescoreArgs& a, cudaStream_t s);
 
@@ -93,7 +97,14 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_tot
                                double* stats, int32_t* level_ws, cudaStream_t s);
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
-                                const void* ovnorm, int32_t* level_ws, cudaStream_t s);
+                                const void* ovnorm, int32_t* level_ws, int which,
+                                cudaStream_t s);
+// exact-decision mode (kern_exact.cu)
+cudaError_t launch_exact_merge_keys(void* pool_k, const Geom& g, float* knorm, const float* oknorm,
+                                    float* shadow, int64_t cap, int32_t* sidx, int32_t* scount,
+                                    int32_t* level_ws, cudaStream_t s);
+cudaError_t launch_convert_rows(const void* src, void* dst, const Geom& g, int32_t* level_ws,
+                                cudaStream_t s);
 cudaError_t launch_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive,
                               int32_t* live, int32_t* rank, int32_t* count, cudaStream_t s);
 cudaError_t launch_stage_rows(const void* pool, int dtype, const Geom& g, int64_t u0, int64_t nU,

@@ -89,8 +89,9 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m, int* til
                        int* partials_per_tile) {
   if (!tile_m || !tile_n || !partials_per_tile) return fail(KVF_ERR_INVALID, "null pointer");
   if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
-  if (path == KVF_PATH_TC) {
-    if (dtype != BF16) return fail(KVF_ERR_INVALID, "tcgen05 path requires a bf16 pool");
+  if (path == KVF_PATH_TC) {  // float32 pools run it on a bf16 operand copy (kvf_convert_rows)
+    if (dtype != BF16 && dtype != F32)
+      return fail(KVF_ERR_INVALID, "tcgen05 path requires a bf16 or float32 pool");
     *tile_m = kTcTileM;
     *tile_n = kTcTileN;
     *partials_per_tile = kTcPartialsPerTile;
@@ -111,6 +112,7 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
                           const int64_t* sample_off, int64_t sample_stride,
                           const int32_t* live, const int32_t* rank, const void* staged,
                           int32_t* rescore_queue, int64_t rescore_cap, double rescore_band,
+                          const void* filter, const float* shadow, const int32_t* sidx,
                           int path, void* stream) {
   SimArgs a;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
@@ -148,7 +150,18 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
     return fail(KVF_ERR_INVALID, "compaction needs live and rank together");
   if (live && !staged && head_mode)
     return fail(KVF_ERR_INVALID, "gathered compaction (no staged rows) needs head_mode 0");
-  if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
+  if ((shadow != nullptr) != (sidx != nullptr))
+    return fail(KVF_ERR_INVALID, "shadow rows and shadow index go together");
+  if (filter && dtype != F32)
+    return fail(KVF_ERR_INVALID, "a bf16 operand copy (filter) is for float32 pools");
+  if (path == KVF_PATH_AUTO) path = (dtype == BF16 || filter) ? KVF_PATH_TC : KVF_PATH_SIMT;
+  if (filter) {  // the tensor cores read the bf16 copy; re-scores read the fp32 pool
+    if (path != KVF_PATH_TC) return fail(KVF_ERR_INVALID, "a filter copy needs the tcgen05 path");
+    a.pool = filter;
+    a.dtype = BF16;
+    a.split3 = 1;
+    if (live) return fail(KVF_ERR_INVALID, "compaction is not available with a float32 split copy");
+  }
   if (live && path != KVF_PATH_TC)
     return fail(KVF_ERR_INVALID, "compacted similarity requires the tcgen05 path");
   if (path == KVF_PATH_TC) {
@@ -169,7 +182,7 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
     if (int rc = cuda_status(launch_sim_tc(a, st), "kvf_similarity_select[tc]")) return rc;
     if (!resc) return KVF_OK;
     RescoreArgs r{pool_k, dtype, a.g, u0, a.resc, a.resc_count, rescore_cap, thr, absorber,
-                  merges, samples, sample_off, sample_stride};
+                  merges, samples, sample_off, sample_stride, shadow, sidx};
     return cuda_status(launch_rescore(r, st), "kvf_similarity_select[rescore]");
   }
   if (path != KVF_PATH_SIMT) return fail(KVF_ERR_INVALID, "unknown path %d", path);
@@ -194,7 +207,7 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB, const uint8_t
 
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t NB, int t, int h,
                      int d, int head_mode, void* knorm, void* vnorm, const void* orig_knorm,
-                     const void* orig_vnorm, int32_t* level_ws, void* stream) {
+                     const void* orig_vnorm, int32_t* level_ws, int which, void* stream) {
   Geom g;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
   if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
@@ -204,9 +217,41 @@ int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t N
   if (r > 16384)
     return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's 16384",
                 (long long)r);
+  if (which < 1 || which > 3) return fail(KVF_ERR_INVALID, "which must be 1 (K), 2 (V) or 3 (K and V)");
   cudaError_t e = launch_merge_groups(pool_k, pool_v, dtype, g, knorm, vnorm, orig_knorm,
-                                      orig_vnorm, level_ws, (cudaStream_t)stream);
+                                      orig_vnorm, level_ws, which, (cudaStream_t)stream);
   return cuda_status(e, "kvf_merge_groups");
+}
+
+int kvf_exact_merge_keys(void* pool_k, int dtype, int64_t L, int64_t NB, int t, int h, int d,
+                         int head_mode, float* knorm, const float* orig_knorm, float* shadow,
+                         int64_t shadow_cap, int32_t* sidx, int32_t* shadow_count,
+                         int32_t* level_ws, void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (dtype != BF16) return fail(KVF_ERR_INVALID, "exact key merge is for bfloat16 pools");
+  if (!pool_k || !knorm || !orig_knorm || !shadow || !sidx || !shadow_count || !level_ws)
+    return fail(KVF_ERR_INVALID, "null pointer");
+  if (d % 8 != 0 || (reinterpret_cast<uintptr_t>(pool_k) & 15) || (reinterpret_cast<uintptr_t>(shadow) & 15))
+    return fail(KVF_ERR_INVALID, "exact key merge needs d %% 8 == 0 and 16-byte aligned buffers");
+  if (g.r() > 16384)
+    return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the exact merge's 16384 "
+                "(use head_mode per_head)", (long long)g.r());
+  return cuda_status(launch_exact_merge_keys(pool_k, g, knorm, orig_knorm, shadow, shadow_cap, sidx,
+                                             shadow_count, level_ws, (cudaStream_t)stream),
+                     "kvf_exact_merge_keys");
+}
+
+int kvf_convert_rows(const void* src, int src_dtype, void* dst, int64_t L, int64_t NB, int t,
+                     int h, int d, int head_mode, int32_t* level_ws, void* stream) {
+  Geom g;
+  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
+  if (src_dtype != F32) return fail(KVF_ERR_INVALID, "convert_rows reads float32 pools");
+  if (!src || !dst) return fail(KVF_ERR_INVALID, "null pointer");
+  if (d % 8 != 0 || (reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15))
+    return fail(KVF_ERR_INVALID, "convert_rows needs d %% 8 == 0 and 16-byte aligned buffers");
+  return cuda_status(launch_convert_rows(src, dst, g, level_ws, (cudaStream_t)stream),
+                     "kvf_convert_rows");
 }
 
 int kvf_alive_rank(int64_t u0, int64_t nU, int64_t NB, const uint8_t* alive, int32_t* live,

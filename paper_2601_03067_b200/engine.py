@@ -26,8 +26,13 @@ from .errors import ConfigError
 from .schedule import Plan
 
 NONE = 0x7FFFFFFF
-# tcgen05 path: pairs with |sim - thr| <= RESCORE_BAND are re-decided in float64
+# tcgen05 path: pairs with |sim - thr| <= band are re-decided in float64.
+# RESCORE_BAND covers the fp32 accumulation of exact bf16 products (level 1 of a
+# bf16 pool: original blocks; float32 pools through the hi/lo split, ~1e-6);
+# RESCORE_BAND_WIDE also covers the bf16 rounding of fused blocks stored in the pool
+# at levels >= 2 in exact mode, |sim_pool - sim_exact| <= ~3e-4 at r = 2048.
 RESCORE_BAND = 2.0**-11
+RESCORE_BAND_WIDE = 2.0**-8
 RESCORE_CAP = 1 << 20
 
 _DT = {torch.float64: N.DT_F64, torch.float32: N.DT_F32, torch.bfloat16: N.DT_BF16}
@@ -153,13 +158,32 @@ class FusionState:
     launches: int = 0
     sim_events: list = field(default_factory=list)  # (start, end, level) CUDA events
     near_threshold: list = field(default_factory=list)  # per level int32[1]: re-scored pairs
+    rescore_cap: int = 0
+    path_name: str = ""  # "tcgen05" | "tcgen05-split3" (float32 hi/lo operands) | "simt"
+    exact: bool = False  # decisions re-scored against float64-derived key directions
+    shadow_count: torch.Tensor | None = None  # int32[1]: shadow slots taken (exact mode)
+    shadow_cap: int = 0
+
+    def inexact_pairs(self) -> int:
+        """Near-threshold pairs that could not be re-scored (queue overflow) and were
+        decided from the tensor-core value; 0 unless a level overflowed RESCORE_CAP."""
+        if not self.rescore_cap:
+            return 0
+        return sum(max(0, int(c.item()) - self.rescore_cap) for c in self.near_threshold)
+
+    def inexact_blocks(self) -> int:
+        """Key absorbers without a shadow row (arena overflow; exact mode only)."""
+        if self.shadow_count is None:
+            return 0
+        return max(0, int(self.shadow_count.item()) - self.shadow_cap)
 
 
 class FusionEngine:
     """Runs fusion of all units of a geometry for one plan (see module doc)."""
 
     def __init__(self, geom: Geometry, plan: Plan, dtype: torch.dtype, device, path: int = N.PATH_AUTO,
-                 compact_from: int | None | str = "auto", compact_mode: str = "auto"):
+                 compact_from: int | None | str = "auto", compact_mode: str = "auto",
+                 exact: bool | None = None):
         if plan.n_blocks != geom.NB:
             raise ConfigError(f"plan covers {plan.n_blocks} blocks, geometry has {geom.NB}")
         self.geom = geom
@@ -167,8 +191,22 @@ class FusionEngine:
         self.dtype = dtype
         self.device = torch.device(device)
         if path == N.PATH_AUTO:
-            path = N.PATH_TC if dtype == torch.bfloat16 and tc_available(geom) else N.PATH_SIMT
+            tc = dtype in (torch.bfloat16, torch.float32) and tc_available(geom)
+            path = N.PATH_TC if tc else N.PATH_SIMT
+        if path == N.PATH_TC and dtype == torch.float64:
+            raise ConfigError("the tcgen05 similarity path takes bf16 or float32 pools")
         self.path = path
+        # float32 pools on the tensor cores: bf16 operand copy + float64 re-score
+        self.filter_mode = path == N.PATH_TC and dtype == torch.float32
+        # exact mode (bf16 pools): fp32 shadow rows of the fused key directions, so
+        # re-scored decisions at levels >= 2 follow the reference's float64 directions
+        if exact is None:
+            exact = path == N.PATH_TC and dtype == torch.bfloat16 and geom.r <= 16384 and geom.d % 8 == 0
+        if exact and not (path == N.PATH_TC and dtype == torch.bfloat16):
+            exact = False  # float32 / float64 pools keep fused keys at full precision already
+        if exact and (geom.r > 16384 or geom.d % 8 != 0):
+            raise ConfigError("exact mode needs r <= 16384 and d % 8 == 0 (use head_mode='per_head')")
+        self.exact = bool(exact)
         self.tm, self.tn, self.ppt = tile_shape(dtype, geom.head_mode, path)
         self.pdev = _plan_device(plan, self.tm, self.tn, self.ppt, self.device)
         U, NB = geom.units, geom.NB
@@ -190,7 +228,7 @@ class FusionEngine:
                 lo = [lv for lv in plan.levels if lv.height == compact_from - 1]
                 if lo and len(lo[0].merges) and int((lo[0].merges[:, 2] - lo[0].merges[:, 0]).min()) >= COMPACT_BIG_MERGE:
                     compact_from -= 1
-        if path != N.PATH_TC or geom.d % 8 != 0:
+        if path != N.PATH_TC or geom.d % 8 != 0 or self.filter_mode:
             compact_from = None
         self.compact_from = compact_from
         # exact float64 re-score of pairs within RESCORE_BAND of the threshold
@@ -198,6 +236,18 @@ class FusionEngine:
         self.rescore_cap = RESCORE_CAP if path == N.PATH_TC else 0
         self.rescore = (torch.empty(4 * (self.rescore_cap + 1), dtype=torch.int32, device=dev)
                         if self.rescore_cap else None)
+        # hi / lo bf16 split of a float32 pool (kvf_convert_rows), 2 x the pool's elements
+        self.filter = (torch.empty(2 * geom.L * NB * geom.E, dtype=torch.bfloat16, device=dev)
+                       if self.filter_mode else None)
+        self.shadow = self.sidx = self.scount = None
+        self.shadow_cap = 0
+        if self.exact:
+            # distinct key absorbers: U * NB / 2 bounds them unless absorbers are themselves
+            # absorbed later; overflow is counted (FusionState.inexact_blocks), never silent
+            self.shadow_cap = max(1, (U * NB + 1) // 2)
+            self.shadow = torch.empty((self.shadow_cap, geom.r), dtype=torch.float32, device=dev)
+            self.sidx = torch.empty((U, NB), dtype=torch.int32, device=dev)
+            self.scount = torch.empty(1, dtype=torch.int32, device=dev)
         # compacted operands: "staged" (dense copy of the alive rows first, one
         # HBM-bound kvf_stage_rows per compacted level) or "gathered" (TMA gather4
         # of the alive rows straight from the pool, folded units; saves the staging
@@ -272,6 +322,19 @@ class FusionEngine:
             g, self.plan, threshold, pool_k, pool_v, knorm, vnorm, oknorm, ovnorm, fusable,
             alive_t, absorber, table_t, ref_t,
         )
+        st.rescore_cap = self.rescore_cap
+        st.path_name = ("simt" if self.path != N.PATH_TC else
+                        "tcgen05-split3" if self.filter_mode else "tcgen05")
+        st.exact = self.exact or self.filter_mode
+        opnd = pool_k  # what the tensor cores read
+        if self.filter is not None:
+            N.call("kvf_convert_rows", N.ptr(pool_k), dt, N.ptr(self.filter), *g.args(), None, sp)
+            opnd = self.filter
+            launches += 1
+        if self.exact:
+            self.sidx.fill_(-1)
+            self.scount.zero_()
+            st.shadow_count, st.shadow_cap = self.scount, self.shadow_cap
         for li, lv in enumerate(self.pdev.levels):
             nm, nt = lv["nm"], lv["nt"]
             stats = torch.empty((U, nm, 8), dtype=torch.float64, device=dev)
@@ -285,13 +348,17 @@ class FusionEngine:
                        N.ptr(self.acount), sp)
                 launches += 1
                 if self.staged is not None:
-                    N.call("kvf_stage_rows", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(self.live),
+                    N.call("kvf_stage_rows", N.ptr(opnd), N.DT_BF16, *g.args(), 0, U, N.ptr(self.live),
                            N.ptr(self.acount), N.ptr(self.staged), sp)
                     launches += 1
             if time_sim:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e1 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
+            # re-score band: the fp32 accumulation error at level 1 of a bf16 pool, plus the
+            # bf16 rounding of the operands where the tensor cores read rounded copies
+            wide = self.exact and self.plan.levels[li].height >= 2
+            band = (RESCORE_BAND_WIDE if wide else RESCORE_BAND) if self.rescore_cap else 0.0
             N.call(
                 "kvf_similarity_select", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(knorm),
                 N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber), N.ptr(lv["merges"]), nm,
@@ -300,8 +367,8 @@ class FusionEngine:
                 samples.shape[1] if samples is not None else 0,
                 N.ptr(self.live) if compact else None, N.ptr(self.rank) if compact else None,
                 N.ptr(self.staged) if compact and self.staged is not None else None,
-                N.ptr(self.rescore), self.rescore_cap,
-                RESCORE_BAND if self.rescore_cap else 0.0, self.path, sp,
+                N.ptr(self.rescore), self.rescore_cap, band,
+                N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx), self.path, sp,
             )
             if self.rescore_cap:
                 launches += 1
@@ -315,10 +382,20 @@ class FusionEngine:
                 N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt,
                 N.ptr(self.partials), N.ptr(stats), N.ptr(self.level_ws), sp,
             )
+            if self.exact:
+                N.call("kvf_exact_merge_keys", N.ptr(pool_k), dt, *g.args(), N.ptr(knorm), N.ptr(oknorm),
+                       N.ptr(self.shadow), self.shadow_cap, N.ptr(self.sidx), N.ptr(self.scount),
+                       N.ptr(self.level_ws), sp)
+                launches += 1
             N.call(
                 "kvf_merge_groups", N.ptr(pool_k), N.ptr(pool_v), dt, *g.args(), N.ptr(knorm),
-                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws), sp,
+                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws),
+                2 if self.exact else 3, sp,
             )
+            if self.filter is not None:  # refresh the bf16 copy of the rewritten keys
+                N.call("kvf_convert_rows", N.ptr(pool_k), dt, N.ptr(self.filter), *g.args(),
+                       N.ptr(self.level_ws), sp)
+                launches += 1
             N.call(
                 "kvf_remap", 0, U, U, NB, N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t),
                 N.ptr(alive_t), N.ptr(self.level_ws), sp,

@@ -43,7 +43,7 @@ def test_argument_errors_map_to_reference_exceptions():
     # invalid threshold / dims are rejected before any CUDA call
     rc = lib.kvf_similarity_select(None, 2, 1, 1, 1, 1, 64, 0, 0, 1, None, None, None, None, None,
                                    0, None, 0, 1.5, None, None, None, 0, None, None, None, None,
-                                   0, 0.0, 1, None)
+                                   0, 0.0, None, None, None, 1, None)
     assert rc == N.KVF_ERR_INVALID
     assert "threshold" in lib.kvf_last_error().decode()
     with pytest.raises(ConfigError):
@@ -53,7 +53,21 @@ def test_argument_errors_map_to_reference_exceptions():
     tm, tn, ppt = C.c_int(), C.c_int(), C.c_int()
     assert lib.kvf_sim_tile_shape(2, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
     assert (tm.value, tn.value, ppt.value) == (256, 256, 16)  # one moment slot per epilogue warp
-    assert lib.kvf_sim_tile_shape(1, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) != 0
+    # float32 pools run the tcgen05 path on a bf16 operand copy; float64 pools cannot
+    assert lib.kvf_sim_tile_shape(1, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
+    assert lib.kvf_sim_tile_shape(0, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) != 0
+    # exact key merge / operand copy validate before any CUDA call
+    rc = lib.kvf_exact_merge_keys(None, 1, 1, 1, 16, 8, 128, 0, None, None, None, 0, None, None,
+                                  None, None)
+    assert rc == N.KVF_ERR_INVALID and "bfloat16" in lib.kvf_last_error().decode()
+    rc = lib.kvf_exact_merge_keys(None, 2, 1, 1, 32, 8, 128, 0, None, None, None, 0, None, None,
+                                  None, None)
+    assert rc == N.KVF_ERR_INVALID
+    rc = lib.kvf_convert_rows(None, 2, None, 1, 1, 16, 8, 128, 0, None, None)
+    assert rc == N.KVF_ERR_INVALID and "float32" in lib.kvf_last_error().decode()
+    rc = lib.kvf_merge_groups(None, None, 2, 1, 1, 16, 8, 128, 0, None, None, None, None, None, 3,
+                              None)
+    assert rc == N.KVF_ERR_INVALID  # null pools
 
 
 def test_schedule_and_compaction_argument_errors():
