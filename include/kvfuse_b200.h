@@ -108,21 +108,6 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           const void* filter, const float* shadow,
                           const int32_t* sidx, int path, void* stream);
 
-/* Exact-decision key merge (bf16 pools; replaces the K half of
- * kvf_merge_groups, fusion.py:259-261 / _unit 285-287 in float64): for each
- * absorber of the level, dir = unit(sum of the members' float64 directions)
- * -- shadow[sidx[j]] for members fused earlier, x_j / |x_j| (float64) of the
- * original block otherwise; dir is kept as an fp32 shadow row (slot taken
- * from *shadow_count on first fusion, up to shadow_cap; overflowing absorbers
- * keep sidx = -1 and the count exceeds the cap) and written to the pool as
- * bf16(s_home * dir) with its stored norm. r <= 16384. */
-int kvf_exact_merge_keys(void* pool_k, int dtype, int64_t L, int64_t NB,
-                         int t, int h, int d, int head_mode, float* knorm,
-                         const float* orig_knorm, float* shadow,
-                         int64_t shadow_cap, int32_t* sidx,
-                         int32_t* shadow_count, int32_t* level_ws,
-                         void* stream);
-
 /* bf16 operand copy of a float32 pool for the tcgen05 similarity: every
  * vector (level_ws == NULL) or the key absorbers of the current level. */
 int kvf_convert_rows(const void* src, int src_dtype, void* dst, int64_t L,
@@ -162,12 +147,20 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB,
  * and the same indices for V (members summed in ascending order); written
  * back as s_home * dir with s_home the home slot's original norm (1 if
  * zero); stored norm recomputed from the rounded values. which: 1 = K only,
- * 2 = V only, 3 = both (the exact-decision mode merges K with
- * kvf_exact_merge_keys). */
+ * 2 = V only, 3 = both.
+ * Exact-decision mode (bf16 pools; shadow != NULL): the key directions follow
+ * the reference's float64 ones -- members fused earlier are read from their
+ * fp32 unit shadow row shadow[sidx[j]] (original blocks as x / |x|), and each
+ * key absorber's new unit direction is written to its row (taken from
+ * *shadow_count on its first fusion, up to shadow_cap; overflowing absorbers
+ * keep sidx = -1 and the count exceeds the cap); the pool still receives
+ * bf16(s_home * dir). r <= 16384. */
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L,
                      int64_t NB, int t, int h, int d, int head_mode, void* knorm,
                      void* vnorm, const void* orig_knorm, const void* orig_vnorm,
-                     int32_t* level_ws, int which, void* stream);
+                     int32_t* level_ws, int which, float* shadow,
+                     int64_t shadow_cap, int32_t* sidx, int32_t* shadow_count,
+                     void* stream);
 
 /* K5 -- block-table remap + refcounts (replaces BlockTable.redirect,
  * core.py:217-227, and alive[rid] = False, fusion.py:262-264); resets the

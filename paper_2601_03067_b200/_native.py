@@ -50,10 +50,6 @@ SIGNATURES: dict[str, tuple] = {
          _vp, _i32, _vp, _i32, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _f64,
          _vp, _vp, _vp, _i32, _vp],
     ),
-    "kvf_exact_merge_keys": (
-        _i32,
-        [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
-    ),
     "kvf_convert_rows": (_i32, [_vp, _i32, _vp, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),
     "kvf_alive_rank": (_i32, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),
     "kvf_stage_rows": (
@@ -66,7 +62,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "kvf_merge_groups": (
         _i32, [_vp, _vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i32,
-               _vp]
+               _vp, _i64, _vp, _vp, _vp]
     ),
     "kvf_remap": (_i32, [_i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp]),
     "kvf_finalize": (

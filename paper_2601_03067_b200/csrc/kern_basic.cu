@@ -57,15 +57,15 @@ __global__ void block_norms_kernel(const T* __restrict__ pool, Geom g,
   const int64_t u = w / g.NB, i = w % g.NB;
   const T* base = pool + g.base(u, i);
   const int64_t nch = g.r() / VEC;
-  A acc = 0;
+  double acc = 0;  // float64 sums: stored norms within an ulp of the reference's (core.py:116)
   for (int64_t c = lane; c < nch; c += 32) {
     A v[VEC];
     VecIO<T, VEC>::load_nc(base + g.off(c * VEC), v);
 #pragma unroll
-    for (int q = 0; q < VEC; ++q) acc += v[q] * v[q];
+    for (int q = 0; q < VEC; ++q) acc = fma((double)v[q], (double)v[q], acc);
   }
   acc = warp_sum(acc);
-  if (lane == 0) norms[w] = sqrt(acc);
+  if (lane == 0) norms[w] = (A)sqrt(acc);
 }
 
 // Per-head units, bf16, d = 128, h = 8: one warp per physical block reads the block's
@@ -81,7 +81,7 @@ __global__ void block_norms_heads_kernel(const __nv_bfloat16* __restrict__ pool,
   const int lane = threadIdx.x & 31;
   if (w >= nblk) return;
   const uint4* base = reinterpret_cast<const uint4*>(pool + w * (int64_t)(T * H * D));
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // float64 sums of exact 8-term fp32 partials
 #pragma unroll 4
   for (int k = 0; k < T * H * D / 8 / 32; ++k) {  // 64 steps of 32 x 16 B
     const uint4 q = __ldg(base + k * 32 + lane);
@@ -98,12 +98,12 @@ __global__ void block_norms_heads_kernel(const __nv_bfloat16* __restrict__ pool,
   const int64_t layer = w / g.NB, blk = w % g.NB;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    float v = acc[j];
+    double v = acc[j];
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // within 16 lanes
     if ((lane & 15) == 0) {
       const int head = 2 * j + (lane >> 4);
-      norms[(layer * H + head) * g.NB + blk] = sqrtf(v);
+      norms[(layer * H + head) * g.NB + blk] = (float)sqrt(v);
     }
   }
 }
@@ -117,7 +117,7 @@ __global__ void block_norms_flat_kernel(const __nv_bfloat16* __restrict__ pool, 
   if (w >= nvec) return;
   const uint4* base = reinterpret_cast<const uint4*>(pool + w * E);
   const int64_t nch = E / 8;
-  float acc = 0.f;
+  double acc = 0.0;  // float64 sums of 8-term fp32 partials (bf16 squares are exact in fp32)
 #pragma unroll 4
   for (int64_t c = lane; c < nch; c += 32) {
     const uint4 q = __ldg(base + c);
@@ -132,7 +132,7 @@ __global__ void block_norms_flat_kernel(const __nv_bfloat16* __restrict__ pool, 
     acc += a;
   }
   acc = warp_sum(acc);
-  if (lane == 0) norms[w] = sqrtf(acc);
+  if (lane == 0) norms[w] = (float)sqrt(acc);
 }
 
 template <typename T>

@@ -258,6 +258,18 @@ struct SlotMeta {
   float home;  // item: original norm of the absorber's home slot
   int32_t gid; // item: global absorber id u * NB + l
   int32_t flags;  // bit0: last vector of the item, bit1: V tensor
+  int32_t sh;  // exact mode, keys: shadow row of this vector (no bulk copy) or -1
+  int32_t ash; // exact mode, keys: the absorber's shadow row (-1: none yet)
+};
+
+// Exact-decision mode (kern_exact.cu): fused key directions live as fp32 shadow
+// rows; members with a row are read from it (unit vectors, inv = 1) and every key
+// absorber's new unit direction is written to its row (allocated on first fusion)
+struct ExactArgs {
+  float* shadow;     // [cap][r] or null (mode off)
+  int64_t cap;
+  int32_t* sidx;     // [U][NB]
+  int32_t* scount;   // rows taken (can exceed cap: overflow is reported)
 };
 
 template <typename T, int EPT>
@@ -265,7 +277,7 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
 merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* __restrict__ knorm,
                  float* __restrict__ vnorm, const float* __restrict__ oknorm,
                  const float* __restrict__ ovnorm, int32_t* ws, int64_t n_total, int nbuf,
-                 int slot_bytes, ItemSel sel) {
+                 int slot_bytes, ItemSel sel, ExactArgs ex) {
   constexpr int VEC = 16 / (int)sizeof(T);
   constexpr int CPT = EPT / VEC;  // 16-byte chunks per consumer thread
   extern __shared__ __align__(128) uint8_t msm[];
@@ -274,6 +286,7 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
   uint64_t* empty = full + MG_MAX_BUF;
   SlotMeta* meta = reinterpret_cast<SlotMeta*>(empty + MG_MAX_BUF);
   float* red = reinterpret_cast<float*>(meta + MG_MAX_BUF);
+  int* slot_bc = reinterpret_cast<int*>(red + 16);
   const LevelWs W(ws, n_total);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = g.r();
@@ -293,8 +306,9 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
     // producer warp: item headers, member ids and their norms are loaded by the
     // whole warp one item ahead, so the copy issue never waits on them
     struct Item {
-      int32_t gid, n, id;  // id / inv: lane k holds vector k of the item (k <= 31)
+      int32_t gid, n, id;  // id / inv / sh: lane k holds vector k of the item (k <= 31)
       float inv, home;
+      int32_t sh;
       bool valid;
     };
     auto load_item = [&](int it) {
@@ -305,6 +319,7 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       x.id = 0;
       x.inv = 0.f;
       x.home = 0.f;
+      x.sh = -1;
       if (!x.valid) return x;
       const bool is_v = sel.is_v(it);
       const float* norm = is_v ? vnorm : knorm;
@@ -317,6 +332,10 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
         x.id = lane == 0 ? (int32_t)(x.gid - gb) : W.members[s0 + lane - 1];
         const float nv = norm[gb + x.id];
         x.inv = nv > 0.f ? 1.f / nv : 0.f;
+        if (ex.shadow && !is_v) {
+          x.sh = ex.sidx[gb + x.id];
+          if (x.sh >= 0) x.inv = 1.f;  // shadow rows are unit directions
+        }
       }
       return x;
     };
@@ -330,16 +349,20 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       const int64_t u = cur.gid / g.NB;
       const int64_t gb = u * g.NB;
       const int s0 = W.mstart[cur.gid];
+      const int32_t ash = __shfl_sync(0xffffffffu, cur.sh, 0);
       for (int v = 0; v <= cur.n; ++v, ++q) {
-        int32_t id;
+        int32_t id, sh;
         float inv;
         if (v < 32) {
           id = __shfl_sync(0xffffffffu, cur.id, v);
           inv = __shfl_sync(0xffffffffu, cur.inv, v);
+          sh = __shfl_sync(0xffffffffu, cur.sh, v);
         } else {  // large groups: beyond the warp-wide prefetch
           id = W.members[s0 + v - 1];
           const float nv = (is_v ? vnorm : knorm)[gb + id];
           inv = nv > 0.f ? 1.f / nv : 0.f;
+          sh = (ex.shadow && !is_v) ? ex.sidx[gb + id] : -1;
+          if (sh >= 0) inv = 1.f;
         }
         if (lane == 0) {
           const int s = q % nbuf;
@@ -349,16 +372,22 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
           mt.home = cur.home;
           mt.gid = cur.gid;
           mt.flags = (v == cur.n ? 1 : 0) | (is_v ? 2 : 0);
+          mt.sh = sh;
+          mt.ash = ash;
           meta[s] = mt;
-          mbar_expect_tx(&full[s], vbytes);  // release: meta visible after the wait
-          const T* src = pool + g.base(u, id);
-          uint8_t* dst = ring + (size_t)s * slot_bytes;
-          if (!g.head_mode) {
-            bulk_g2s(dst, src, vbytes, &full[s]);
+          if (sh >= 0) {  // consumers read the shadow row from global memory
+            mbar_arrive(&full[s]);
           } else {
-            const uint32_t segb = (uint32_t)(g.d * sizeof(T));
-            for (int tk = 0; tk < g.t; ++tk)
-              bulk_g2s(dst + tk * segb, src + (int64_t)tk * g.h * g.d, segb, &full[s]);
+            mbar_expect_tx(&full[s], vbytes);  // release: meta visible after the wait
+            const T* src = pool + g.base(u, id);
+            uint8_t* dst = ring + (size_t)s * slot_bytes;
+            if (!g.head_mode) {
+              bulk_g2s(dst, src, vbytes, &full[s]);
+            } else {
+              const uint32_t segb = (uint32_t)(g.d * sizeof(T));
+              for (int tk = 0; tk < g.t; ++tk)
+                bulk_g2s(dst + tk * segb, src + (int64_t)tk * g.h * g.d, segb, &full[s]);
+            }
           }
         }
       }
@@ -381,14 +410,32 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       mbar_wait(&full[s], (q / nbuf) & 1);
       mt = meta[s];
       const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * slot_bytes);
+      if (mt.sh >= 0) {  // exact mode: fused member, its fp32 unit direction
+        const float* row = ex.shadow + (int64_t)mt.sh * r;
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
-        if (c < nch) {
-          float x[VEC];
-          VecIO<T, VEC>::load(sp + c * VEC, x);
+        for (int k = 0; k < CPT; ++k) {
+          const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+          if (c < nch) {
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) acc[k * VEC + e] = fmaf(x[e], mt.inv, acc[k * VEC + e]);
+            for (int e4 = 0; e4 < VEC; e4 += 4) {
+              const float4 f = __ldg(reinterpret_cast<const float4*>(row + c * VEC + e4));
+              acc[k * VEC + e4 + 0] += f.x;
+              acc[k * VEC + e4 + 1] += f.y;
+              acc[k * VEC + e4 + 2] += f.z;
+              acc[k * VEC + e4 + 3] += f.w;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+          const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+          if (c < nch) {
+            float x[VEC];
+            VecIO<T, VEC>::load(sp + c * VEC, x);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[k * VEC + e] = fmaf(x[e], mt.inv, acc[k * VEC + e]);
+          }
         }
       }
       __syncwarp();
@@ -407,12 +454,36 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
     const float nrm = sqrtf(consumer_sum(ss, red));
     const float sc = nrm > 0.f ? (mt.home > 0.f ? mt.home : 1.f) / nrm : 0.f;
     T* xl = pool + g.base(u, l);
+    // exact mode, keys: the absorber's shadow row (taken on its first fusion)
+    float* srow = nullptr;
+    const float inv_n = nrm > 0.f ? 1.f / nrm : 0.f;
+    if (ex.shadow && !is_v) {
+      if (ct == 0) {
+        int sl = mt.ash;
+        if (sl < 0) {
+          sl = atomicAdd(ex.scount, 1);
+          if (sl < ex.cap) ex.sidx[mt.gid] = sl; else sl = -1;
+        }
+        *slot_bc = sl;
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+      const int sl = *slot_bc;
+      asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+      if (sl >= 0) srow = ex.shadow + (int64_t)sl * r;
+    }
     float rs = 0.f;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
       const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
       if (c < nch) {
         float y[VEC], rd[VEC];
+        if (srow) {
+#pragma unroll
+          for (int e4 = 0; e4 < VEC; e4 += 4)
+            *reinterpret_cast<float4*>(srow + c * VEC + e4) =
+                make_float4(acc[k * VEC + e4] * inv_n, acc[k * VEC + e4 + 1] * inv_n,
+                            acc[k * VEC + e4 + 2] * inv_n, acc[k * VEC + e4 + 3] * inv_n);
+        }
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = acc[k * VEC + e] * sc;
         VecIO<T, VEC>::store(xl + g.off(c * VEC), y, rd);
@@ -770,8 +841,8 @@ cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, con
 template <typename T, int EPT>
 cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
                       const void* ovn, int32_t* ws, int64_t n_total, int nbuf, int slot_bytes, ItemSel sel,
-                      cudaStream_t s) {
-  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + MG_MAX_BUF * (int)sizeof(SlotMeta) + 64;
+                      ExactArgs ex, cudaStream_t s) {
+  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + MG_MAX_BUF * (int)sizeof(SlotMeta) + 128;
   static int attr = 0;  // per instantiation
   if (attr < smem) {
     cudaError_t e = cudaFuncSetAttribute(merge_tma_kernel<T, EPT>,
@@ -795,14 +866,14 @@ cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, con
   }();
   merge_tma_kernel<T, EPT><<<per_sm * n_sm, MG_THREADS, smem, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn,
                                                          (const float*)okn, (const float*)ovn, ws,
-                                                         n_total, nbuf, slot_bytes, sel);
+                                                         n_total, nbuf, slot_bytes, sel, ex);
   return cudaGetLastError();
 }
 
 template <typename T>
 cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
                            const void* ovn, int32_t* ws, int64_t n_total, ItemSel sel,
-                           cudaStream_t s) {
+                           ExactArgs ex, cudaStream_t s) {
   constexpr int VEC = Vec16<T>::N;
   const int64_t r = g.r();
   const int64_t vbytes = r * (int64_t)sizeof(T);
@@ -819,7 +890,30 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
   const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
+  if (ex.shadow) {  // exact mode (bf16 pools, keys)
+    if (!std::is_same<T, __nv_bfloat16>::value) return cudaErrorInvalidValue;
+    if (!(tma_ok && !g.head_mode && (sel.which & 1))) {
+      // keys on the float64 CTA-per-absorber kernel, values below on the usual path
+      if (sel.which & 1) {
+        cudaError_t e = launch_exact_merge_keys(pk, g, (float*)kn, (const float*)okn, ex.shadow, ex.cap,
+                                                ex.sidx, ex.scount, ws, s);
+        if (e != cudaSuccess || sel.which == 1) return e;
+      }
+      sel = ItemSel{2};
+      ex = ExactArgs{nullptr, 0, nullptr, nullptr};
+    }
+  }
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    if (ex.shadow) {  // folded exact mode: keys and values in one ring pass
+      const int64_t ept = (r + MG_CONSUMERS - 1) / MG_CONSUMERS;
+      if (ept <= 8)
+        return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
+      if (ept <= 16)
+        return merge_tma<T, 16>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
+      if (ept <= 32)
+        return merge_tma<T, 32>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
+      return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
+    }
     // per-head units of 2 or 4 KB: warp per item, per-warp smem ring (3 slots)
     if (g.head_mode && (vbytes == 4096 || vbytes == 2048) && g.t <= 32 && (g.d * 2) % 16 == 0 &&
         can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g) && !getenv("KVF_MERGE_NO_RING")) {
@@ -855,12 +949,12 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
     if (tma_ok) {
       const int64_t ept = (r + MG_CONSUMERS - 1) / MG_CONSUMERS;
       if (ept <= 8)
-        return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
+        return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
       if (ept <= 16)
-        return merge_tma<T, 16>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
+        return merge_tma<T, 16>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
       if (ept <= 32)
-        return merge_tma<T, 32>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
-      return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, s);
+        return merge_tma<T, 32>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
+      return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
     }
   }
   if (can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g))
@@ -871,21 +965,23 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
 
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
-                                const void* ovnorm, int32_t* level_ws, int which,
-                                cudaStream_t s) {
+                                const void* ovnorm, int32_t* level_ws, int which, float* shadow,
+                                int64_t shadow_cap, int32_t* sidx, int32_t* scount, cudaStream_t s) {
   if (which < 1 || which > 3) return cudaErrorInvalidValue;
   const ItemSel sel{which};
+  const ExactArgs ex{shadow, shadow_cap, sidx, scount};
+  if (shadow && dtype != BF16) return cudaErrorInvalidValue;
   const int64_t n_total = g.units() * g.NB;
   switch (dtype) {
     case F64:
       return merge_dispatch<double>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, level_ws,
-                                    n_total, sel, s);
+                                    n_total, sel, ex, s);
     case F32:
       return merge_dispatch<float>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm, level_ws,
-                                   n_total, sel, s);
+                                   n_total, sel, ex, s);
     default:
       return merge_dispatch<__nv_bfloat16>(pool_k, pool_v, g, knorm, vnorm, oknorm, ovnorm,
-                                           level_ws, n_total, sel, s);
+                                           level_ws, n_total, sel, ex, s);
   }
 }
 

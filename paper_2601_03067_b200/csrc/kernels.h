@@ -97,8 +97,8 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_tot
                                double* stats, int32_t* level_ws, cudaStream_t s);
 cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geom& g,
                                 void* knorm, void* vnorm, const void* oknorm,
-                                const void* ovnorm, int32_t* level_ws, int which,
-                                cudaStream_t s);
+                                const void* ovnorm, int32_t* level_ws, int which, float* shadow,
+                                int64_t shadow_cap, int32_t* sidx, int32_t* scount, cudaStream_t s);
 // exact-decision mode (kern_exact.cu)
 cudaError_t launch_exact_merge_keys(void* pool_k, const Geom& g, float* knorm, const float* oknorm,
                                     float* shadow, int64_t cap, int32_t* sidx, int32_t* scount,

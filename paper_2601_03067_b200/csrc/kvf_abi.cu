@@ -207,7 +207,8 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB, const uint8_t
 
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t NB, int t, int h,
                      int d, int head_mode, void* knorm, void* vnorm, const void* orig_knorm,
-                     const void* orig_vnorm, int32_t* level_ws, int which, void* stream) {
+                     const void* orig_vnorm, int32_t* level_ws, int which, float* shadow,
+                     int64_t shadow_cap, int32_t* sidx, int32_t* shadow_count, void* stream) {
   Geom g;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
   if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
@@ -218,28 +219,17 @@ int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t N
     return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's 16384",
                 (long long)r);
   if (which < 1 || which > 3) return fail(KVF_ERR_INVALID, "which must be 1 (K), 2 (V) or 3 (K and V)");
+  if (shadow) {
+    if (dtype != BF16) return fail(KVF_ERR_INVALID, "exact mode (shadow rows) is for bfloat16 pools");
+    if (!sidx || !shadow_count) return fail(KVF_ERR_INVALID, "shadow rows need sidx and shadow_count");
+    if (d % 8 != 0 || (reinterpret_cast<uintptr_t>(pool_k) & 15) ||
+        (reinterpret_cast<uintptr_t>(shadow) & 15))
+      return fail(KVF_ERR_INVALID, "exact mode needs d %% 8 == 0 and 16-byte aligned buffers");
+  }
   cudaError_t e = launch_merge_groups(pool_k, pool_v, dtype, g, knorm, vnorm, orig_knorm,
-                                      orig_vnorm, level_ws, which, (cudaStream_t)stream);
+                                      orig_vnorm, level_ws, which, shadow, shadow_cap, sidx,
+                                      shadow_count, (cudaStream_t)stream);
   return cuda_status(e, "kvf_merge_groups");
-}
-
-int kvf_exact_merge_keys(void* pool_k, int dtype, int64_t L, int64_t NB, int t, int h, int d,
-                         int head_mode, float* knorm, const float* orig_knorm, float* shadow,
-                         int64_t shadow_cap, int32_t* sidx, int32_t* shadow_count,
-                         int32_t* level_ws, void* stream) {
-  Geom g;
-  if (int rc = check_geom(L, NB, t, h, d, head_mode, &g)) return rc;
-  if (dtype != BF16) return fail(KVF_ERR_INVALID, "exact key merge is for bfloat16 pools");
-  if (!pool_k || !knorm || !orig_knorm || !shadow || !sidx || !shadow_count || !level_ws)
-    return fail(KVF_ERR_INVALID, "null pointer");
-  if (d % 8 != 0 || (reinterpret_cast<uintptr_t>(pool_k) & 15) || (reinterpret_cast<uintptr_t>(shadow) & 15))
-    return fail(KVF_ERR_INVALID, "exact key merge needs d %% 8 == 0 and 16-byte aligned buffers");
-  if (g.r() > 16384)
-    return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the exact merge's 16384 "
-                "(use head_mode per_head)", (long long)g.r());
-  return cuda_status(launch_exact_merge_keys(pool_k, g, knorm, orig_knorm, shadow, shadow_cap, sidx,
-                                             shadow_count, level_ws, (cudaStream_t)stream),
-                     "kvf_exact_merge_keys");
 }
 
 int kvf_convert_rows(const void* src, int src_dtype, void* dst, int64_t L, int64_t NB, int t,

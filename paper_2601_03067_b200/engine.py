@@ -382,15 +382,10 @@ class FusionEngine:
                 N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt,
                 N.ptr(self.partials), N.ptr(stats), N.ptr(self.level_ws), sp,
             )
-            if self.exact:
-                N.call("kvf_exact_merge_keys", N.ptr(pool_k), dt, *g.args(), N.ptr(knorm), N.ptr(oknorm),
-                       N.ptr(self.shadow), self.shadow_cap, N.ptr(self.sidx), N.ptr(self.scount),
-                       N.ptr(self.level_ws), sp)
-                launches += 1
             N.call(
                 "kvf_merge_groups", N.ptr(pool_k), N.ptr(pool_v), dt, *g.args(), N.ptr(knorm),
-                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws),
-                2 if self.exact else 3, sp,
+                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws), 3,
+                N.ptr(self.shadow), self.shadow_cap, N.ptr(self.sidx), N.ptr(self.scount), sp,
             )
             if self.filter is not None:  # refresh the bf16 copy of the rewritten keys
                 N.call("kvf_convert_rows", N.ptr(pool_k), dt, N.ptr(self.filter), *g.args(),

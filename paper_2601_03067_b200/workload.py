@@ -29,15 +29,23 @@ def _layer_blocks(gen: torch.Generator, n: int, r: int, assign: torch.Tensor, n_
 
 def synthetic_kv(L: int, B: int, p: int, t: int, h: int, d: int, *, dtype=torch.bfloat16,
                  seed: int = 0, variant: str = "bff", c_lo: float = 0.80, c_hi: float = 0.99,
-                 cluster_div: int = 4, device=None) -> tuple[torch.Tensor, torch.Tensor]:
+                 cluster_div: int = 4, device=None, layers=None) -> tuple[torch.Tensor, torch.Tensor]:
     """K, V of shape (L, B, p, t, h, d). BFF: B*p/4 clusters per layer shared
-    across requests; CFF: p/4 clusters per request (chunks of one request)."""
+    across requests; CFF: p/4 clusters per request (chunks of one request).
+
+    Every layer has its own generator seeded from (seed, layer), so `layers`
+    (a subset of range(L)) returns exactly those layers of the full cache,
+    shape (len(layers), B, p, t, h, d) -- how bench.py hands the CPU reference
+    the same bytes the GPU fused."""
     device = torch.device(device or "cuda")
     r = t * h * d
     n = B * p
-    K = torch.empty((L, B, p, t, h, d), dtype=dtype, device=device)
+    layers = list(range(L)) if layers is None else [int(x) for x in layers]
+    if any(not 0 <= x < L for x in layers):
+        raise ValueError(f"layers must lie in [0, {L})")
+    K = torch.empty((len(layers), B, p, t, h, d), dtype=dtype, device=device)
     V = torch.empty_like(K)
-    for layer in range(L):
+    for out_i, layer in enumerate(layers):
         gen = torch.Generator(device=device)
         gen.manual_seed((seed * 1_000_003 + layer * 7919) & 0x7FFF_FFFF_FFFF)
         if variant == "bff":
@@ -50,7 +58,7 @@ def synthetic_kv(L: int, B: int, p: int, t: int, h: int, d: int, *, dtype=torch.
                       + torch.arange(B, device=device)[:, None] * per).reshape(-1)
         for out in (K, V):
             blk = _layer_blocks(gen, n, r, assign, nc, c_lo, c_hi, device)
-            out[layer].copy_(blk.reshape(B, p, t, h, d).to(dtype))
+            out[out_i].copy_(blk.reshape(B, p, t, h, d).to(dtype))
     return K, V
 
 

@@ -56,18 +56,18 @@ def test_argument_errors_map_to_reference_exceptions():
     # float32 pools run the tcgen05 path on a bf16 operand copy; float64 pools cannot
     assert lib.kvf_sim_tile_shape(1, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
     assert lib.kvf_sim_tile_shape(0, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) != 0
-    # exact key merge / operand copy validate before any CUDA call
-    rc = lib.kvf_exact_merge_keys(None, 1, 1, 1, 16, 8, 128, 0, None, None, None, 0, None, None,
-                                  None, None)
-    assert rc == N.KVF_ERR_INVALID and "bfloat16" in lib.kvf_last_error().decode()
-    rc = lib.kvf_exact_merge_keys(None, 2, 1, 1, 32, 8, 128, 0, None, None, None, 0, None, None,
-                                  None, None)
-    assert rc == N.KVF_ERR_INVALID
+    # exact-mode merge / operand copy validate before any CUDA call
     rc = lib.kvf_convert_rows(None, 2, None, 1, 1, 16, 8, 128, 0, None, None)
     assert rc == N.KVF_ERR_INVALID and "float32" in lib.kvf_last_error().decode()
     rc = lib.kvf_merge_groups(None, None, 2, 1, 1, 16, 8, 128, 0, None, None, None, None, None, 3,
-                              None)
+                              None, 0, None, None, None)
     assert rc == N.KVF_ERR_INVALID  # null pools
+    x = C.c_int()
+    p = C.addressof(x)
+    rc = lib.kvf_merge_groups(p, p, 1, 1, 1, 16, 8, 128, 0, p, p, p, p, p, 3, p, 1, p, p, None)
+    assert rc == N.KVF_ERR_INVALID and "bfloat16" in lib.kvf_last_error().decode()
+    rc = lib.kvf_merge_groups(p, p, 2, 1, 1, 16, 8, 128, 0, p, p, p, p, p, 4, None, 0, None, None, None)
+    assert rc == N.KVF_ERR_INVALID and "which" in lib.kvf_last_error().decode()
 
 
 def test_schedule_and_compaction_argument_errors():

@@ -17,14 +17,18 @@ pytestmark = pytest.mark.gpu
 K = pytest.importorskip("paper_2601_03067_b200")
 from paper_2601_03067_b200.workload import synthetic_kv  # noqa: E402
 
-# epsilon of the near-threshold exemption and direction tolerances per dtype
-EPS = {torch.float32: 2e-5, torch.bfloat16: 1e-3}
-# reported similarity samples: bf16 tiles carry the tensor-core fp32
-# accumulation error (~1e-4 relative at r = 16K); decisions near the
-# threshold are re-scored exactly, so for bf16 EPS covers the bf16 storage of
-# fused directions at levels >= 2 (up to ~2.5e-4 observed at r = 2048; it
-# shrinks ~1/sqrt(r)), with the usual 4x margin
-SAMPLE_TOL = {torch.float32: 5e-6, torch.bfloat16: 5e-4}
+# epsilon of the near-threshold exemption: decisions are exact on both dtypes
+# (bf16: exact mode, float64 re-score against fp32 shadow rows of the fused keys;
+# float32: hi/lo split on the tensor cores + float64 re-score of the band), so
+# only pairs within 1e-9 of the threshold may be adopted, and none may flip
+EPS = {torch.float32: 1e-9, torch.bfloat16: 1e-9}
+MAX_FLIPS = 0
+# reported similarity samples carry the tensor-core accumulation error (the
+# UMMA fp32 accumulator is not IEEE-exact: up to ~1e-4 relative, the same for
+# float32 pools through the hi/lo split -- 7.1e-5 observed -- as for bf16 inputs
+# at level 1) and, for bf16, the bf16 storage of fused blocks at levels >= 2
+# (~2.5e-4 observed at r = 2048); re-scored pairs carry float64 values
+SAMPLE_TOL = {torch.float32: 3e-4, torch.bfloat16: 5e-4}
 DIR_TOL = {torch.float32: 2e-6, torch.bfloat16: 2.0**-8}
 # bf16 directions are re-rounded at every level they are rewritten
 DIR_RTOL = {torch.float32: 0.0, torch.bfloat16: 2.0**-7}
@@ -83,6 +87,7 @@ def test_bff_vs_oracle(dtype, head_mode, thr, d):
                           B, p, thr, gpu_absorber=st.absorber[oc.fused.unit].cpu().numpy(), eps=EPS[dtype])
         _compare_unit(oc, ref, dtype)
         flips += ref.flips
+    assert flips <= MAX_FLIPS
     assert sum(o.report.blocks_after for o in outs) < sum(o.report.blocks_before for o in outs)
 
 

@@ -59,8 +59,8 @@ def test_tc_matches_simt_and_oracle(shape, head_mode):
     for u in range(geom.units):
         layer, head = (u // h, u % h) if head_mode else (u, None)
         ref = O.fuse_unit(O.layer_unit(Kh, layer, head), O.layer_unit(Vh, layer, head), B, p, 0.8,
-                          gpu_absorber=st_tc.absorber[u].cpu().numpy(), eps=1e-4, keep_samples=False)
-        assert ref.mismatches == 0, ref.mismatch_detail
+                          gpu_absorber=st_tc.absorber[u].cpu().numpy(), eps=1e-9, keep_samples=False)
+        assert ref.mismatches == 0 and ref.flips == 0, ref.mismatch_detail  # exact mode
         np.testing.assert_array_equal(st_tc.table[u].cpu().numpy(), ref.table)
         np.testing.assert_array_equal(st_tc.refcount[u].cpu().numpy(), ref.refcount)
 
