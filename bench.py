@@ -394,6 +394,7 @@ def reference_main(args):
     per = total / len(layers)
     layer_bytes = kv_bytes(c, 2 if c["dtype"] == "bf16" else 4) / c["L"]
     value = layer_bytes / per / 1e9
+    P = max(len(w) for w in waves)
     sample = (f"{len(layers)} steps = layers {layers[0]}..{layers[-1]} of the {c['workload']} cache at full shape "
               f"({c['B']} requests x {c['p'] * c['t']} tokens, seed {GPU_SEED}: rank 0's bytes), {P} layers at a "
               f"time in {len(waves)} wave(s), one layer per thread, float64 reference engine, OPENBLAS_NUM_THREADS=1")

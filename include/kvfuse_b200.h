@@ -171,7 +171,8 @@ int kvf_remap(int64_t u0, int64_t nU, int64_t U, int64_t NB,
 
 /* Finalize: per-slot scales k_scale[s] = orig_knorm[s] / knorm[table[s]]
  * (same for V; refold semantics core.py:303-304), ascending live list
- * (FusedLayer.phys_ids, fusion.py:316) and ascending free list per unit. */
+ * (FusedLayer.phys_ids, fusion.py:316) and ascending free list per unit.
+ * live_ids == NULL: scales only (after a BlockTable mutation). */
 int kvf_finalize(int dtype, int64_t u0, int64_t nU, int64_t NB,
                  const void* orig_knorm, const void* orig_vnorm,
                  const void* knorm, const void* vnorm, const int32_t* table,

@@ -295,7 +295,10 @@ def _attention_fused(query: AttentionQuery, fused: FusedCache, row: int):
     ks[u, :bpr] = st.k_scale[u, sl]
     vs[u, :bpr] = st.v_scale[u, sl]
     kv_head = fused.head if g.head_mode else query.head
-    return _single(query, st.pool_k, st.pool_v, g, fused.layer, table, ks, vs, bpr, kv_head, g.h)
+    # the kernel indexes layers of the run's own pool: fused.layer is the user-facing
+    # index (fast_fusion's layer=, or the cache layer of a streamed chunk)
+    local_layer = u // g.h if g.head_mode else u
+    return _single(query, st.pool_k, st.pool_v, g, local_layer, table, ks, vs, bpr, kv_head, g.h)
 
 
 def _single(query, pool_k, pool_v, geom, layer, table, ks, vs, p_blocks, kv_head, h):

@@ -275,7 +275,7 @@ class _RefcountView(MutableMapping):
 
     def __setitem__(self, phys, value):
         self._t._refcount[int(phys)] = int(value)
-        self._t._dirty()
+        self._t._mutated()
 
     def __delitem__(self, phys):
         alive, _, _ = self._host()
@@ -283,7 +283,7 @@ class _RefcountView(MutableMapping):
             raise KeyError(phys)
         self._t._refcount[int(phys)] = 0
         self._t._alive[int(phys)] = 0
-        self._t._dirty()
+        self._t._mutated()
 
     def __iter__(self):
         alive, _, _ = self._host()
@@ -320,7 +320,7 @@ class _EntriesView(MutableMapping):
     def __setitem__(self, slot, phys):
         i, j = slot
         self._t._table[i * self._t.blocks_per_row + j] = int(phys)
-        self._t._dirty()
+        self._t._mutated()
 
     def __delitem__(self, slot):
         raise CorruptionError("logical slots cannot be removed from a paged block table")
@@ -356,6 +356,7 @@ class BlockTable:
         self._alive = alive
         self.reusable: set[int] = set()
         self._cache = None
+        self._listeners: list = []  # called after a mutation (derived per-slot scales)
 
     @classmethod
     def identity(cls, layer: int, rows: int, blocks_per_row: int, device=None) -> "BlockTable":
@@ -371,6 +372,14 @@ class BlockTable:
     # -- host mirror -------------------------------------------------------
     def _dirty(self):
         self._cache = None
+
+    def _mutated(self):
+        """A slot or refcount changed (redirect, entries / refcount writes): drop the
+        host mirror and let dependents (the fused unit's per-slot K / V scales,
+        K_s = key_norm[s] / |x_table[s]| * x_table[s]) recompute on the device."""
+        self._cache = None
+        for fn in self._listeners:
+            fn()
 
     def _host_state(self):
         if self._cache is None:
@@ -437,7 +446,7 @@ class BlockTable:
             "kvf_table_redirect", n, N.ptr(self._table), N.ptr(self._refcount), N.ptr(self._alive),
             int(from_phys), int(to_phys), N.ptr(bad), N.stream_ptr(),
         )
-        self._dirty()
+        self._mutated()
         if int(bad.item()):
             raise CorruptionError(f"dangling physical block id in redirect({from_phys}, {to_phys})")
 

@@ -500,6 +500,7 @@ def _outcomes_from_state(st: FusionState, keep_samples: bool, rows: int, bpr: in
             table = tables[u]
         else:
             table = BlockTable(layer, rows, bpr, st.table[u], st.refcount[u], st.alive[u])
+        table._listeners.append(lambda u=u: _refresh_scales(st, u))
         fused = FusedCache(
             keys=FusedLayer(phys, loader=lambda f=loader: f(st.pool_k, st.knorm)),
             values=FusedLayer(phys, loader=lambda f=loader: f(st.pool_v, st.vnorm)),
@@ -526,6 +527,18 @@ def _outcomes_from_state(st: FusionState, keep_samples: bool, rows: int, bpr: in
         )
         outcomes.append(FusionOutcome(fused=fused, report=report))
     return outcomes
+
+
+def _refresh_scales(st: FusionState, u: int) -> None:
+    """Per-slot K / V scales of unit u from its current table (kvf_finalize without the
+    live / free lists: the FusedCache keeps its post-fusion survivors, as the
+    reference's frozen FusedLayer does after a later BlockTable.redirect)."""
+    g = st.geom
+    N.call(
+        "kvf_finalize", dtype_code(st.pool_k.dtype), u, 1, g.NB, N.ptr(st.orig_knorm),
+        N.ptr(st.orig_vnorm), N.ptr(st.knorm), N.ptr(st.vnorm), N.ptr(st.table), N.ptr(st.alive),
+        N.ptr(st.k_scale), N.ptr(st.v_scale), None, None, None, None, N.stream_ptr(),
+    )
 
 
 def _want_samples(keep_samples, plan: Plan, units: int) -> bool:
@@ -696,7 +709,10 @@ def fast_fusion(keys: UnfoldedLayer, values: UnfoldedLayer, thr: float,
     # the pool holds raw blocks: direction * norm (reference keeps them split)
     pk = (kvec.to(acc) * kn.to(acc)[..., None]).to(kvec.dtype).contiguous().reshape(-1)
     pv = (vvec.to(acc) * vn.to(acc)[..., None]).to(vvec.dtype).contiguous().reshape(-1)
-    geom = Geometry(1, rows * bpr, 1, 1, r, 0)
+    # the pool holds each row as a (t, h, d) block when the caller names one (attention
+    # over the fused unit reads heads), else as one r-vector
+    bt, bh, bd = block_shape if block_shape and int(np.prod(block_shape)) == r else (1, 1, r)
+    geom = Geometry(1, rows * bpr, int(bt), int(bh), int(bd), 0)
     plan = single_tree_plan(rows, bpr)
     engine = FusionEngine(geom, plan, pk.dtype, dev, path)
     ks = _want_samples(keep_samples, plan, 1)
