@@ -37,7 +37,7 @@ from .core import (
     default_device,
 )
 from .engine import NONE, FusionEngine, FusionState, Geometry, acc_dtype, dtype_code
-from .errors import ConfigError, InsufficientDataError, InvalidCacheError
+from .errors import ConfigError, CorruptionError, InsufficientDataError, InvalidCacheError
 from .schedule import Plan, bff_plan, cff_plan, single_tree_plan
 
 SAMPLES_AUTO_LIMIT = 1 << 22  # pairs across all units and levels
@@ -632,7 +632,21 @@ def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_p
     return out
 
 
-def _outcomes(runs, keep_samples, rows, bpr, shape) -> list[FusionOutcome]:
+def _audit_runs(runs) -> None:
+    """Post-fusion table audit of every unit (the reference audits each layer after
+    fusion, fusion.py:305 / 315, core.py:232-241): refcounts must equal the slot
+    counts and only live blocks may be referenced. One device pass per run."""
+    from .engine import audit
+
+    for st, _ in runs:
+        g = st.geom
+        if not audit(st.table, st.refcount, st.alive, g.units, g.NB):
+            raise CorruptionError("refcounts inconsistent with logical slot mapping")
+
+
+def _outcomes(runs, keep_samples, rows, bpr, shape, check: bool = True) -> list[FusionOutcome]:
+    if check:
+        _audit_runs(runs)
     outs: list[FusionOutcome] = []
     for st, c0 in runs:
         outs.extend(_outcomes_from_state(st, keep_samples, rows, bpr, shape, layer_offset=c0))
@@ -640,11 +654,14 @@ def _outcomes(runs, keep_samples, rows, bpr, shape) -> list[FusionOutcome]:
 
 
 def fuse_batch(cache: PagedKvCache, cfg: FusionConfig, *, in_place: bool = False,
-               keep_samples: bool | None = None, path: int = N.PATH_AUTO) -> list[FusionOutcome]:
+               keep_samples: bool | None = None, path: int = N.PATH_AUTO,
+               audit: bool = True) -> list[FusionOutcome]:
     """Batch Fast-Fusion across requests, all layers at once (fusion.py:360-374).
 
     Returns one outcome per layer (folded) or per (layer, kv head) in
-    per-head mode, layer-major.
+    per-head mode, layer-major. ``audit`` runs the device table audit after
+    fusion and raises CorruptionError on an inconsistent table, as the
+    reference does per layer (fusion.py:315).
     """
     if cfg.variant != "bff":
         raise ConfigError(f"fuse_batch requires variant 'bff', got {cfg.variant!r}")
@@ -655,12 +672,12 @@ def fuse_batch(cache: PagedKvCache, cfg: FusionConfig, *, in_place: bool = False
     ks = _want_samples(keep_samples, plan, geom.units)
     runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path)
     shape = (dims.t, 1, dims.d) if hm else (dims.t, dims.h, dims.d)
-    return _outcomes(runs, ks, dims.B, dims.p, shape)
+    return _outcomes(runs, ks, dims.B, dims.p, shape, check=audit)
 
 
 def fuse_chunks(cache: PagedKvCache, cfg: FusionConfig, chunk_tokens: int, *,
                 in_place: bool = False, keep_samples: bool | None = None,
-                path: int = N.PATH_AUTO) -> list[FusionOutcome]:
+                path: int = N.PATH_AUTO, audit: bool = True) -> list[FusionOutcome]:
     """Chunks Fast-Fusion across the chunks of each request (fusion.py:377-415).
 
     Rows are (request, chunk); trees never cross requests; physical blocks
@@ -676,7 +693,7 @@ def fuse_chunks(cache: PagedKvCache, cfg: FusionConfig, chunk_tokens: int, *,
     ks = _want_samples(keep_samples, plan, geom.units)
     runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path)
     shape = (dims.t, 1, dims.d) if hm else (dims.t, dims.h, dims.d)
-    outcomes = _outcomes(runs, ks, dims.B * C, bpc, shape)
+    outcomes = _outcomes(runs, ks, dims.B * C, bpc, shape, check=audit)
     for oc in outcomes:  # reusable = {refcount > 1} (fusion.py:409-411)
         ref = oc.fused.table.device_refcount.cpu().numpy()
         oc.fused.table.reusable = set(int(p) for p in np.nonzero(ref > 1)[0])
@@ -732,6 +749,7 @@ def fast_fusion(keys: UnfoldedLayer, values: UnfoldedLayer, thr: float,
                     keep_samples=ks, **kw)
     if table is not None:
         table._dirty()
+    _audit_runs([(st, 0)])  # fusion.py:305 (table.audit after the tree)
     shape = block_shape or (1, 1, r)
     return _outcomes_from_state(st, ks, rows, bpr, shape, tables=tables, layer_override=layer)[0]
 
