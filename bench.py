@@ -459,7 +459,8 @@ def ours_main(args):
     Kw, Vw = torch.empty_like(K0), torch.empty_like(V0)
     engine = FusionEngine(geom, plan, dtype, dev, {"auto": N.PATH_AUTO, "tc": N.PATH_TC,
                                                   "simt": N.PATH_SIMT}[args.path],
-                          exact={"auto": None, "on": True, "off": False}[args.exact])
+                          exact={"auto": None, "on": True, "off": False}[args.exact],
+                          split=not args.no_split)
     U = geom.units
     gathered = torch.empty((world, U), dtype=torch.int32, device=dev)
 
@@ -1074,6 +1075,7 @@ def main():
                     help="eager launches of the fusion step")
     ap.add_argument("--exact", choices=["auto", "on", "off"], default="auto",
                     help="exact-decision mode (fp32 shadow rows of fused keys; default on for bf16)")
+    ap.add_argument("--no-split", action="store_true", help="disable split-K similarity (A/B)")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--ref-layers", type=int, default=8,
                     help="layers of the GPU arm's cache the CPU reference fuses for the parity / "

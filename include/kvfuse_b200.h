@@ -93,8 +93,11 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m,
  * float64 recomputation in the same call; NULL / 0 disables it.
  * filter (float32 pools): bf16 copy of the pool (kvf_convert_rows) that the
  *   tensor cores read; the re-score reads the float32 pool.
- * shadow / sidx (exact mode, kvf_exact_merge_keys): the re-score reads a fused
- *   key from its fp32 shadow row instead of the rounded pool block. */
+ * shadow / sidx (exact mode, kvf_merge_groups): the re-score reads a fused
+ *   key from its fp32 shadow row instead of the rounded pool block.
+ * nsplit > 1 (tcgen05 path): split-K over each tile's k-steps for levels with
+ *   few, long-K tiles; split_part = float[nt * nU * nsplit * 65536] partials,
+ *   split_count = int32[nt * nU * 2] zeroed once (left at zero on exit). */
 int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           int t, int h, int d, int head_mode, int64_t u0,
                           int64_t nU, const void* knorm, const uint8_t* fusable,
@@ -106,7 +109,8 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB,
                           const void* staged, int32_t* rescore_queue,
                           int64_t rescore_cap, double rescore_band,
                           const void* filter, const float* shadow,
-                          const int32_t* sidx, int path, void* stream);
+                          const int32_t* sidx, int nsplit, float* split_part,
+                          int32_t* split_count, int path, void* stream);
 
 /* bf16 operand copy of a float32 pool for the tcgen05 similarity: every
  * vector (level_ws == NULL) or the key absorbers of the current level. */

@@ -48,7 +48,7 @@ SIGNATURES: dict[str, tuple] = {
         _i32,
         [_vp, _i32, _i64, _i64, _i32, _i32, _i32, _i32, _i64, _i64, _vp, _vp, _vp, _vp,
          _vp, _i32, _vp, _i32, _f64, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _f64,
-         _vp, _vp, _vp, _i32, _vp],
+         _vp, _vp, _vp, _i32, _vp, _vp, _i32, _vp],
     ),
     "kvf_convert_rows": (_i32, [_vp, _i32, _vp, _i64, _i64, _i32, _i32, _i32, _i32, _vp, _vp]),
     "kvf_alive_rank": (_i32, [_i64, _i64, _i64, _vp, _vp, _vp, _vp, _vp]),

@@ -135,6 +135,27 @@ __global__ void block_norms_flat_kernel(const __nv_bfloat16* __restrict__ pool, 
   if (lane == 0) norms[w] = (float)sqrt(acc);
 }
 
+// Folded units, float32: the same warp-per-block stream (four 16-B loads in flight)
+__global__ void block_norms_flat_f32_kernel(const float* __restrict__ pool, int64_t nvec, int64_t E,
+                                            float* __restrict__ norms) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= nvec) return;
+  const float4* base = reinterpret_cast<const float4*>(pool + w * E);
+  const int64_t nch = E / 4;
+  double acc = 0.0;
+#pragma unroll 4
+  for (int64_t c = lane; c < nch; c += 32) {
+    const float4 q = __ldg(base + c);
+    acc = fma((double)q.x, (double)q.x, acc);
+    acc = fma((double)q.y, (double)q.y, acc);
+    acc = fma((double)q.z, (double)q.z, acc);
+    acc = fma((double)q.w, (double)q.w, acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) norms[w] = (float)sqrt(acc);
+}
+
 template <typename T>
 static cudaError_t norms_t(const void* pool, const Geom& g, void* norms, cudaStream_t s) {
   using A = typename AccOf<T>::type;
@@ -151,6 +172,13 @@ static cudaError_t norms_t(const void* pool, const Geom& g, void* norms, cudaStr
     if (!g.head_mode && g.E() % 8 == 0 && (reinterpret_cast<uintptr_t>(pool) & 15) == 0) {
       block_norms_flat_kernel<<<(unsigned)blocks, 256, 0, s>>>((const __nv_bfloat16*)pool, nvec, g.E(),
                                                                (float*)norms);
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (std::is_same<T, float>::value) {
+    if (!g.head_mode && g.E() % 4 == 0 && (reinterpret_cast<uintptr_t>(pool) & 15) == 0) {
+      block_norms_flat_f32_kernel<<<(unsigned)blocks, 256, 0, s>>>((const float*)pool, nvec, g.E(),
+                                                                   (float*)norms);
       return cudaGetLastError();
     }
   }

@@ -245,8 +245,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               const int64_t* __restrict__ sample_off, int64_t sample_stride,
               const int32_t* __restrict__ live, const int32_t* __restrict__ rank,
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
-              float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3) {
+              float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3,
+              int nsplit, float* __restrict__ spart, int32_t* __restrict__ scnt) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ int split_last_sh;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint8_t* meta = smem + STAGES * STAGE_BYTES;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta);
@@ -267,7 +269,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   const uint32_t crank = cta_rank();
   const bool leader = crank == 0;
   const bool staged = live != nullptr;  // tiles index alive positions (staged or gathered rows)
-  const int nwork = (int)(nt * nU);
+  // split-K (few, long-K tiles: cfg1 / CFF levels): work item = (tile, k-split); each
+  // split's fp32 accumulator goes to spart, the CTA arriving last per (tile, CTA rank)
+  // sums the nsplit partials in split order (deterministic) and runs the epilogue
+  const int nwork = (int)(nt * nU) * nsplit;
   const int P = (int)(gridDim.x >> 1);
   const int layer_div = g.head_mode ? g.h : 1;
   const int dpc = g.d / BK;
@@ -326,8 +331,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         break;
       }
       const TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
+      const int sk = sched_rec[sl * kRec + 10];
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
+      const int kr0 = (int)((int64_t)sk * nk_run / nsplit), kr1 = (int)((int64_t)(sk + 1) * nk_run / nsplit);
       const int layer = (int)(t.u / layer_div);
       const int head = g.head_mode ? (int)(t.u % g.h) : 0;
       const int mi0 = t.i0 + (int)crank * BM;
@@ -365,7 +372,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int rowB =
           (staged ? (int)(t.ul * g.NB) + t.pm + t.j0 : layer * g.NB + t.mid + t.j0) +
           (int)crank * BNH;
-      for (int kr = 0; kr < nk_run; ++kr, ++kk) {
+      for (int kr = kr0; kr < kr1; ++kr, ++kk) {
         const int s = kk % STAGES;
         const uint32_t ph = (kk / STAGES) & 1;
         mbar_wait(&empty_bar[s], ph ^ 1);
@@ -400,9 +407,9 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
             w = -1;
             break;
           }
-          t0 = tile_info(w, nt, u0, g, merges, tiles, rank, staged);
+          t0 = tile_info(w / nsplit, nt, u0, g, merges, tiles, rank, staged);
           if (t0.active) break;
-          const int tile = w - (int)t0.ul * nt;  // tile fully beyond the alive blocks
+          const int tile = w / nsplit - (int)t0.ul * nt;  // tile fully beyond the alive blocks
           double* pp = partials + ((int64_t)t0.ul * nt + tile) * kTcPartialsPerTile * 5;
           for (int q = 0; q < kTcPartialsPerTile; ++q) {
             pp[5 * q + 0] = pp[5 * q + 1] = pp[5 * q + 2] = 0.0;
@@ -410,14 +417,15 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
             pp[5 * q + 4] = -INFINITY;
           }
         }
-        int32_t r[kRec] = {w, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        // r[0] = tile work id (w / nsplit), r[10] = k-split
+        int32_t r[kRec] = {w < 0 ? -1 : w / nsplit, 0, 0, 0, 0, 0, 0, 0, 0, 0, w < 0 ? 0 : w % nsplit, 0};
         if (w >= 0) {
           r[1] = t0.m; r[2] = t0.i0; r[3] = t0.j0; r[4] = t0.lb; r[5] = t0.mid; r[6] = t0.re;
           r[7] = t0.pl; r[8] = t0.pm; r[9] = t0.pr;
         }
         int32_t* dst = sched_rec + sl * kRec;
 #pragma unroll
-        for (int q = 0; q < 10; ++q) {
+        for (int q = 0; q < 11; ++q) {
           dst[q] = r[q];
           st_cluster_s32(dst + q, 1, r[q]);
         }
@@ -433,13 +441,15 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         const int sl = it % SCHED_DEPTH;
         mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
         const int w = sched_rec[sl * kRec];
+        const int sk = sched_rec[sl * kRec + 10];
         mbar_arrive_cluster(&sched_empty[sl], 0);
         if (w < 0) break;
+        const int nks = (int)((int64_t)(sk + 1) * nk_run / nsplit) - (int)((int64_t)sk * nk_run / nsplit);
         const uint32_t acc = tc & 1;
         mbar_wait_cluster(&tmem_empty[acc], ((tc >> 1) & 1) ^ 1);  // epilogue drained it
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dst = tmem_base + acc * BN;
-        for (int ks = 0; ks < nk_run; ++ks, ++kk) {
+        for (int ks = 0; ks < nks; ++ks, ++kk) {
           const int s = kk % STAGES;
           const uint32_t ph = (kk / STAGES) & 1;
           mbar_wait(&full_bar[s], ph);
@@ -483,6 +493,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int sl = it % SCHED_DEPTH;
       mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
       const int w = sched_rec[sl * kRec];
+      const int sk = sched_rec[sl * kRec + 10];
       const TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
@@ -527,6 +538,58 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const uint32_t acc = tc & 1;
       mbar_wait(&tmem_full[acc], (tc >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (nsplit > 1) {
+        // this split's partial accumulator -> spart[(tile, split, CTA)][col][row]
+        // (column-major: a warp's 32 rows are one 128-B line per column)
+        float* mine = spart + (((int64_t)w * nsplit + sk) * 2 + crank) * (int64_t)(BM * BN);
+        for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) mine[(int64_t)(c0 + c) * BM + row] = __uint_as_float(v[c]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);  // accumulator free already
+        __threadfence();
+        asm volatile("bar.sync 2, %0;" ::"n"(ET) : "memory");
+        if (et == 0) {
+          int32_t* cp = scnt + (int64_t)w * 2 + crank;
+          const int old = atomicAdd(cp, 1);
+          split_last_sh = old == nsplit - 1;
+          if (old == nsplit - 1) *cp = 0;  // reset for the next launch
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(ET) : "memory");
+        const bool last = split_last_sh != 0;
+        __threadfence();
+        if (!last) {  // another split of this tile finishes it; no moments, no decisions
+          ++tc;
+          continue;
+        }
+      }
+      // accumulator chunk c0 of this thread's row: TMEM, or the sum of the tile's
+      // split partials in split order (bitwise reproducible)
+      auto load_acc = [&](int c0, uint32_t (&v)[32]) {
+        if (nsplit == 1) {
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
+          return;
+        }
+        const float* p0 = spart + ((int64_t)w * nsplit * 2 + crank) * (int64_t)(BM * BN) +
+                          (int64_t)c0 * BM + row;
+        float a[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) a[c] = 0.f;
+        for (int s = 0; s < nsplit; ++s) {  // 32 independent L2 loads in flight per split
+          const float* ps = p0 + (int64_t)s * 2 * BM * BN;
+          float x[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) x[c] = __ldcg(ps + (int64_t)c * BM);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) a[c] += x[c];
+        }
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(a[c]);
+      };
       // pairs with s > tlo take the slow path: threshold decision, or deferral
       // of near-threshold pairs to the exact float64 re-score (the tensor-core
       // fp32 accumulation over r/16 steps can be off by ~1e-4 relative)
@@ -565,7 +628,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       };
       for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
         uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
+        load_acc(c0, v);
         // columns of this chunk that take part (alive, fusable, inside the merge)
         const unsigned okm = __ballot_sync(0xffffffffu, ok_j[c0 + lane] != 0);
         if (ok_i) cnt += __popc(okm);
@@ -620,10 +683,12 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
           mx = fmaxf(mx, inv_i * rmx);
         }
       }
-      // accumulator drained: hand the buffer back to the MMA warp
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+      // accumulator drained: hand the buffer back to the MMA warp (split tiles did above)
+      if (nsplit == 1) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+      }
       ++tc;
       // this warp's similarity moments -> its own slot (fp32 warp tree, fixed order)
 #pragma unroll
@@ -789,7 +854,9 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
     }
     max_clusters = n;
   }
-  const int64_t nwork = (int64_t)a.nt * a.nU;
+  const int nsplit = a.nsplit > 1 && !gathered ? a.nsplit : 1;
+  if (nsplit > 1 && (!a.split_part || !a.split_count)) return cudaErrorInvalidValue;
+  const int64_t nwork = (int64_t)a.nt * a.nU * nsplit;
   if (nwork + max_clusters >= INT32_MAX) return cudaErrorInvalidValue;
   int32_t* counter = work_counter(s);
   if (counter == nullptr) return cudaErrorMemoryAllocation;
@@ -797,7 +864,8 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
       tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
-      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? 1 : 0, split3 ? 1 : 0);
+      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? 1 : 0, split3 ? 1 : 0,
+      nsplit, a.split_part, a.split_count);
   return cudaGetLastError();
 }
 

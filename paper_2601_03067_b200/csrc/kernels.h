@@ -45,6 +45,12 @@ struct SimArgs {
   double resc_band = 0.0;
   // float32 pools: `pool` is the hi/lo bf16 split copy (2 * L * NB rows, kvf_convert_rows)
   int split3 = 0;
+  // split-K over the k-steps of each tile (nsplit > 1): fp32 partials
+  // [nt * nU][nsplit][2][256][128] and per-(tile, CTA) arrival counters [nt * nU][2]
+  // (zero-initialised once; the kernel leaves them at zero)
+  int nsplit = 1;
+  float* split_part = nullptr;
+  int32_t* split_count = nullptr;
 };
 
 struct RescoreArgs {

@@ -113,6 +113,7 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
                           const int32_t* live, const int32_t* rank, const void* staged,
                           int32_t* rescore_queue, int64_t rescore_cap, double rescore_band,
                           const void* filter, const float* shadow, const int32_t* sidx,
+                          int nsplit, float* split_part, int32_t* split_count,
                           int path, void* stream) {
   SimArgs a;
   if (int rc = check_geom(L, NB, t, h, d, head_mode, &a.g)) return rc;
@@ -152,6 +153,12 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
     return fail(KVF_ERR_INVALID, "gathered compaction (no staged rows) needs head_mode 0");
   if ((shadow != nullptr) != (sidx != nullptr))
     return fail(KVF_ERR_INVALID, "shadow rows and shadow index go together");
+  if (nsplit < 1 || nsplit > 64) return fail(KVF_ERR_INVALID, "nsplit must lie in [1, 64]");
+  if (nsplit > 1 && (!split_part || !split_count))
+    return fail(KVF_ERR_INVALID, "split-K needs the partials buffer and the arrival counters");
+  a.nsplit = nsplit;
+  a.split_part = split_part;
+  a.split_count = split_count;
   if (filter && dtype != F32)
     return fail(KVF_ERR_INVALID, "a bf16 operand copy (filter) is for float32 pools");
   if (path == KVF_PATH_AUTO) path = (dtype == BF16 || filter) ? KVF_PATH_TC : KVF_PATH_SIMT;

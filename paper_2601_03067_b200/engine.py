@@ -183,7 +183,7 @@ class FusionEngine:
 
     def __init__(self, geom: Geometry, plan: Plan, dtype: torch.dtype, device, path: int = N.PATH_AUTO,
                  compact_from: int | None | str = "auto", compact_mode: str = "auto",
-                 exact: bool | None = None):
+                 exact: bool | None = None, split: bool = True):
         if plan.n_blocks != geom.NB:
             raise ConfigError(f"plan covers {plan.n_blocks} blocks, geometry has {geom.NB}")
         self.geom = geom
@@ -239,6 +239,28 @@ class FusionEngine:
         # hi / lo bf16 split of a float32 pool (kvf_convert_rows), 2 x the pool's elements
         self.filter = (torch.empty(2 * geom.L * NB * geom.E, dtype=torch.bfloat16, device=dev)
                        if self.filter_mode else None)
+        # split-K per level (tcgen05 path): few, long-K tiles (cfg1, CFF) spread over all SMs
+        self.nsplit = [1] * len(self.pdev.levels)
+        self.split_part = self.split_count = None
+        if path == N.PATH_TC and split:
+            pairs = max(1, torch.cuda.get_device_properties(self.device).multi_processor_count // 2)
+            nk = geom.r // 64 * (3 if self.filter_mode else 1)
+            need, tiles_max = 0, 0
+            for li, lv in enumerate(self.pdev.levels):
+                compacted = compact_from is not None and plan.levels[li].height >= compact_from
+                if compacted and compact_mode == "gathered":
+                    continue
+                n_tiles = lv["nt"] * U
+                s = choose_split(n_tiles, nk, pairs)
+                while s > 1 and n_tiles * s * _TILE_PART_BYTES > SPLIT_PART_BUDGET:
+                    s -= 1
+                self.nsplit[li] = s
+                if s > 1:
+                    need = max(need, n_tiles * s * _TILE_PART_BYTES)
+                    tiles_max = max(tiles_max, n_tiles)
+            if need:
+                self.split_part = torch.empty(need // 4, dtype=torch.float32, device=dev)
+                self.split_count = torch.zeros(2 * tiles_max, dtype=torch.int32, device=dev)
         self.shadow = self.sidx = self.scount = None
         self.shadow_cap = 0
         if self.exact:
@@ -368,7 +390,9 @@ class FusionEngine:
                 N.ptr(self.live) if compact else None, N.ptr(self.rank) if compact else None,
                 N.ptr(self.staged) if compact and self.staged is not None else None,
                 N.ptr(self.rescore), self.rescore_cap, band,
-                N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx), self.path, sp,
+                N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx),
+                self.nsplit[li], N.ptr(self.split_part) if self.nsplit[li] > 1 else None,
+                N.ptr(self.split_count) if self.nsplit[li] > 1 else None, self.path, sp,
             )
             if self.rescore_cap:
                 launches += 1
@@ -416,6 +440,25 @@ class FusionEngine:
 
 
 COMPACT_BIG_MERGE = 65536  # blocks per merge (left + right)
+SPLIT_PART_BUDGET = 512 << 20  # bytes of split-K partials per engine
+_TILE_PART_BYTES = 256 * 256 * 4  # one CTA pair's fp32 accumulator tile
+
+
+def choose_split(n_tiles: int, nk_run: int, pairs: int) -> int:
+    """k-splits per tile for a similarity launch: levels with at most half a wave of
+    tiles and long K (folded units: r / 64 k-steps, x3 for float32 hi/lo operands) are
+    split so every CTA pair has work; cost model = waves of (tile, split) items x split
+    length, +2% per split for the partial write / read-back. Measured: cfg1 (16 / 8 / 4
+    tiles, 768 k-steps) similarity 0.93 -> 0.35 ms per step; fuller levels (cfg3 level 1:
+    128 tiles, HBM-bound) lose, so they are never split."""
+    if n_tiles <= 0 or 2 * n_tiles > pairs or nk_run < 64:
+        return 1
+    best, best_cost = 1, float(-(-n_tiles // pairs))
+    for s in range(2, min(16, nk_run // 32) + 1):
+        cost = -(-(n_tiles * s) // pairs) / s * (1.0 + 0.02 * s)
+        if cost < best_cost - 1e-9:
+            best, best_cost = s, cost
+    return best
 
 
 class CapturedFusion:

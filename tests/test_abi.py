@@ -43,7 +43,7 @@ def test_argument_errors_map_to_reference_exceptions():
     # invalid threshold / dims are rejected before any CUDA call
     rc = lib.kvf_similarity_select(None, 2, 1, 1, 1, 1, 64, 0, 0, 1, None, None, None, None, None,
                                    0, None, 0, 1.5, None, None, None, 0, None, None, None, None,
-                                   0, 0.0, None, None, None, 1, None)
+                                   0, 0.0, None, None, None, 1, None, None, 1, None)
     assert rc == N.KVF_ERR_INVALID
     assert "threshold" in lib.kvf_last_error().decode()
     with pytest.raises(ConfigError):
