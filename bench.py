@@ -10,9 +10,10 @@ levels) starting from the pristine pool.
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
 
-Multi-GPU: weak scaling -- every rank fuses its own cache (distinct seed);
-fusion has no exchange, NCCL all-gathers the per-layer compression counters
-inside each step (the only collective on the path).
+Multi-GPU: strong scaling -- one cache; rank r fuses its contiguous layer shard
+(dist.shard_units; layers are independent, fusion.py:367-374). Inside every
+timed step NCCL all-gathers the per-unit block counts and gathers the remapped
+tables to rank 0 -- the path's only collectives.
 """
 
 from __future__ import annotations
@@ -156,6 +157,19 @@ def all_gather_rows(dist, out, mine):
         dist.all_gather(parts, mine.cpu())
         for r, t in enumerate(parts):
             out[r].copy_(t)
+
+
+def gather_rows(dist, out_list, mine, dst=0):
+    """dist.gather of one tensor per rank to `dst` (NCCL: device tensors; gloo test hook:
+    host copies)."""
+    if dist_backend() == "nccl":
+        dist.gather(mine, out_list, dst=dst)
+    else:
+        parts = [t.cpu() for t in out_list] if out_list is not None else None
+        dist.gather(mine.cpu(), parts, dst=dst)
+        if out_list is not None:
+            for o, t in zip(out_list, parts):
+                o.copy_(t)
 
 
 def kv_bytes(c, elem):
@@ -410,7 +424,7 @@ def reference_main(args):
                        "cache (imports, allocator); the numpy reference has no other warm-up state",
         "ms_per_step": per * 1e3,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": f"synthetic ({c['dtype']} values of the GPU arm's generator, widened to float64)",
@@ -435,6 +449,7 @@ def ours_main(args):
     from paper_2601_03067_b200 import CacheDims, FusionConfig, PagedKvCache, fuse_batch, fuse_chunks
     from paper_2601_03067_b200 import _native as N
     from paper_2601_03067_b200.core import cff_layout
+    from paper_2601_03067_b200.dist import shard_units
     from paper_2601_03067_b200.engine import RESCORE_BAND, RESCORE_BAND_WIDE, FusionEngine, Geometry
     from paper_2601_03067_b200.schedule import bff_plan, cff_plan
     from paper_2601_03067_b200.workload import synthetic_kv
@@ -449,20 +464,30 @@ def ours_main(args):
     elem = 2 if dtype == torch.bfloat16 else 4
     hm = 1 if args.head_mode == "per_head" else 0
     L, B, p, t, h, d = c["L"], c["B"], c["p"], c["t"], c["h"], c["d"]
-    geom = Geometry(L, B * p, t, h, d, hm)
+    # strong scaling: one cache (seed GPU_SEED) of L layers; rank r fuses its contiguous
+    # layer shard (layers are independent, fusion.py:367-374) -- N = 1 fuses all of them
+    shard = shard_units(L, world, rank)
+    Ll = len(shard)
+    upl = h if hm else 1  # units per layer
+    geom = Geometry(Ll, B * p, t, h, d, hm)
     if c["variant"] == "cff":
         C, bpc = cff_layout(p, t, c["chunk_tokens"])
         plan = cff_plan(B, C, bpc, None)
     else:
         plan = bff_plan(B, p, None)
-    K0, V0 = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=GPU_SEED + rank, variant=c["variant"], device=dev)
+    K0, V0 = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=GPU_SEED, variant=c["variant"], device=dev,
+                          layers=list(shard))
     Kw, Vw = torch.empty_like(K0), torch.empty_like(V0)
     engine = FusionEngine(geom, plan, dtype, dev, {"auto": N.PATH_AUTO, "tc": N.PATH_TC,
                                                   "simt": N.PATH_SIMT}[args.path],
                           exact={"auto": None, "on": True, "off": False}[args.exact],
                           split=not args.no_split)
     U = geom.units
-    gathered = torch.empty((world, U), dtype=torch.int32, device=dev)
+    n_max = -(-L // world) * upl  # units of the largest shard (collective buffers are padded)
+    live_pad = torch.zeros(n_max, dtype=torch.int32, device=dev)
+    tab_pad = torch.zeros((n_max, geom.NB), dtype=torch.int32, device=dev)
+    gathered = torch.zeros((world, n_max), dtype=torch.int32, device=dev)
+    tables_dst = [torch.empty_like(tab_pad) for _ in range(world)] if (rank == 0 and world > 1) else None
 
     graph = None
     graph_note = "eager launches"
@@ -484,10 +509,15 @@ def ours_main(args):
             st = graph.replay()
         else:
             st = engine.run(Kw.view(-1), Vw.view(-1), c["thr"], time_sim=timed)
-        if world > 1:  # the path's only collective: gather per-unit block counts
-            all_gather_rows(dist, gathered, st.live_count)
+        # the path's only collectives: all-gather the per-unit block counts,
+        # gather every rank's remapped tables to rank 0
+        live_pad[:U].copy_(st.live_count)
+        if world > 1:
+            all_gather_rows(dist, gathered, live_pad)
+            tab_pad[:U].copy_(st.table)
+            gather_rows(dist, tables_dst, tab_pad)
         else:
-            gathered[0].copy_(st.live_count)
+            gathered[0].copy_(live_pad)
         e1.record()
         return e0, e1, st
 
@@ -511,6 +541,7 @@ def ours_main(args):
     # similarity kernel timing for the roofline: the timed steps' own CUDA events;
     # a graph replay has none, so one extra (untimed) eager step is measured instead
     sim_recs = recs
+    st_e = None
     if graph is not None:  # as many eager steps as timed ones (steady state, not one cold run)
         sim_recs = []
         for _ in range(args.steps):
@@ -540,8 +571,8 @@ def ours_main(args):
     total_ms = float(tmax.item())
     ms_per_step = total_ms / args.steps
     live = gathered.sum().item()
-    cr = (world * U * geom.NB) / live
-    value = world * kv_bytes(c, elem) / (ms_per_step / 1e3) / 1e9
+    cr = (L * upl * geom.NB) / live
+    value = kv_bytes(c, elem) / (ms_per_step / 1e3) / 1e9  # the whole cache, all ranks
 
     out = None
     if rank == 0:
@@ -570,14 +601,16 @@ def ours_main(args):
             "warmup": args.warmup,
             "ms_per_step": ms_per_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": c["dtype"],
-            "data": "synthetic clustered KV (SURVEY §8d generator, seed 1000+rank)",
+            "data": f"synthetic clustered KV (SURVEY §8d generator, seed {GPU_SEED}), each rank generates its layers",
             "config": {
                 "workload": c["workload"], "L": L, "B": B, "p": p, "t": t, "h": h, "d": d,
                 "threshold": c["thr"], "variant": c["variant"], "head_mode": args.head_mode,
-                "parallelism": f"replicas x{world} (weak; layer units independent, NCCL gathers counters)",
+                "parallelism": (f"layer-sharded x{world}: ranks fuse {[len(shard_units(L, world, r)) for r in range(world)]} "
+                                f"of the {L} layers; per step NCCL all_gather of the per-unit block counts + "
+                                "gather of the remapped int32 tables to rank 0 (inside the timed region)"),
                 "l2": f"inputs {kv_bytes(c, elem) / 1e9:.1f} GB >> 126 MB L2; pristine-pool restore copy "
                       "between steps (untimed)",
                 "timing": "sum of per-step CUDA-event intervals on the launch stream, max over ranks; "
@@ -632,7 +665,10 @@ def ours_main(args):
         if rank == 0:
             out["e2e"] = e2e
     # ---- decode over a BFF-fused cache vs the unfused cache (K6, BASELINE configs[3]) ----
-    del recs, st_last, K0, V0, Kw, Vw, engine
+    # the captured graph keeps its private memory pool (engine buffers allocated during
+    # capture: shadow rows, staging, per-level stats) until it is released
+    del recs, st_last, K0, V0, Kw, Vw, engine, graph, sim_recs, st_e
+    torch.cuda.synchronize()
     torch.cuda.empty_cache()
     torch._C._host_emptyCache()  # release the e2e leg's pinned host buffers before the CPU legs
     if rank == 0 and not args.skip_decode:
@@ -1048,7 +1084,8 @@ def bench_e2e(args, c, K0, V0, dtype, dev, world, torch, dist, PagedKvCache, Cac
         ok = int(flag.item())
     if not ok:
         return {"value": None, "unit": "GB/s", "error": why or "a peer rank could not pin its host buffers"}
-    dims = CacheDims(B=c["B"], p=c["p"], t=c["t"], h=c["h"], d=c["d"], L=c["L"])
+    # this rank's layer shard as its own host-resident cache (N = 1: the whole cache)
+    dims = CacheDims(B=c["B"], p=c["p"], t=c["t"], h=c["h"], d=c["d"], L=int(K0.shape[0]))
     cfg = FusionConfig(threshold=c["thr"], variant=c["variant"], head_mode=args.head_mode)
 
     def once():
@@ -1079,8 +1116,17 @@ def bench_e2e(args, c, K0, V0, dtype, dev, world, torch, dist, PagedKvCache, Cac
         reduce_max(dist, dt)
     per = float(dt.item())
     elem = 2 if dtype == torch.bfloat16 else 4
-    return {"value": world * kv_bytes(c, elem) / per / 1e9, "unit": "GB/s",
-            "h2d_bytes_per_step": kv_bytes(c, elem), "d2h_bytes_per_step": d2h,
+    d2h_t = torch.tensor([d2h], dtype=torch.float64, device=dev)
+    if world > 1:  # bytes of all ranks (d2h differs by shard size)
+        if dist_backend() == "nccl":
+            dist.all_reduce(d2h_t)
+        else:
+            hh = d2h_t.cpu()
+            dist.all_reduce(hh)
+            d2h_t.copy_(hh)
+    return {"value": kv_bytes(c, elem) / per / 1e9, "unit": "GB/s",
+            "h2d_bytes_per_step": kv_bytes(c, elem), "d2h_bytes_per_step": int(d2h_t.item()),
+            "bytes_note": "all ranks: each streams its layer shard of the cache",
             "ms_per_step": per * 1e3, "steps": steps,
             "path": "PagedKvCache(pinned host, defer_upload) -> fuse_batch(in_place; H2D streamed "
                     "in 4-layer chunks under fusion) -> table/refcount/scales .cpu()"}

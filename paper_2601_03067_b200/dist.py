@@ -64,3 +64,50 @@ def gather_tables(table: torch.Tensor, dst: int = 0, group=None) -> list[torch.T
     if rank != dst:
         return None
     return [b[: int(s.item())] for b, s in zip(bufs, sizes)]
+
+
+def _coll_device(group=None) -> torch.device:
+    """Tensors for collectives: CUDA for NCCL, host for gloo."""
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
+@dataclass
+class ShardedFusion:
+    """One rank's share of a layer-sharded fusion run (fuse_batch_sharded)."""
+
+    layers: range  # this rank's layers of the cache
+    outcomes: list  # FusionOutcome per local unit (layer, or layer x kv head)
+    stats: CompressionStats  # all ranks: aggregate blocks before / after, per-rank after
+    tables: list[torch.Tensor] | None  # on `dst`: every rank's int32 tables [units_r, NB]
+
+
+def fuse_batch_sharded(cache, cfg, *, group=None, gather: bool = True, dst: int = 0,
+                       **kwargs) -> ShardedFusion:
+    """BFF (or CFF with cfg.variant == "cff" and chunk_tokens=) over the layers of this
+    rank's shard (fusion.py:367-374: layers are independent), then the path's only
+    collectives: an all-gather of the per-unit block counts and, with `gather`, a
+    gather of the remapped int32 tables to `dst`. Every rank holds the whole cache
+    description; only its layers are read (device caches: views; host-resident
+    caches: only these layers are streamed). Returns this rank's ShardedFusion."""
+    from .fusion import fuse_batch, fuse_chunks
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    mine = shard_units(cache.dims.L, world, rank)
+    chunk_tokens = kwargs.pop("chunk_tokens", None)
+    if cfg.variant == "cff":
+        outs = fuse_chunks(cache, cfg, chunk_tokens, layers=mine, **kwargs)
+    else:
+        outs = fuse_batch(cache, cfg, layers=mine, **kwargs)
+    cd = _coll_device(group)
+    before = torch.tensor([o.report.blocks_before for o in outs], dtype=torch.int64, device=cd)
+    after = torch.tensor([o.report.blocks_after for o in outs], dtype=torch.int64, device=cd)
+    stats = gather_compression(before, after, group=group)
+    tables = None
+    if gather:
+        local = torch.stack([o.fused.table.device_table for o in outs]).to(cd)
+        tables = gather_tables(local, dst=dst, group=group)
+    return ShardedFusion(mine, outs, stats, tables)

@@ -548,10 +548,11 @@ def _want_samples(keep_samples, plan: Plan, units: int) -> bool:
     return total <= SAMPLES_AUTO_LIMIT
 
 
-def _pools(cache: PagedKvCache, in_place: bool):
+def _pools(cache: PagedKvCache, in_place: bool, l0: int = 0, l1: int | None = None):
+    k, v = cache.keys_dev[l0:l1], cache.values_dev[l0:l1]
     if in_place:
-        return cache.keys_dev, cache.values_dev
-    return cache.keys_dev.clone(), cache.values_dev.clone()
+        return k, v
+    return k.clone(), v.clone()
 
 
 def _head_mode(cfg: FusionConfig) -> int:
@@ -578,33 +579,51 @@ def _stream_chunks(L: int) -> list[tuple[int, int]]:
     return out
 
 
-def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_place: bool,
-                keep_samples: bool, path: int) -> list[tuple[FusionState, int]]:
-    """Fuse every unit of the cache; returns (state, first layer) per engine run.
+def _layer_range(layers, L: int) -> tuple[int, int]:
+    """(first, stop) of a contiguous layer selection (a range, e.g. dist.shard_units)."""
+    if layers is None:
+        return 0, L
+    ls = list(layers)
+    if not ls:
+        raise ConfigError("layers selects no layer")
+    l0, l1 = ls[0], ls[-1] + 1
+    if ls != list(range(l0, l1)) or l0 < 0 or l1 > L:
+        raise ConfigError(f"layers must be a contiguous range inside [0, {L}), got {layers!r}")
+    return l0, l1
 
-    Device-resident caches run as one engine pass. Host-resident caches
+
+def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_place: bool,
+                keep_samples: bool, path: int, layers=None) -> list[tuple[FusionState, int]]:
+    """Fuse the units of the selected layers (all by default); returns (state, first
+    layer) per engine run.
+
+    Device-resident caches run as one engine pass over the layer range (a view of
+    the pool: layers are the outermost dimension). Host-resident caches
     (PagedKvCache(..., defer_upload=True)) stream to the GPU in chunks of
     STREAM_LAYERS layers on a copy stream while earlier chunks fuse on the
     current stream; every chunk is validated for NaN / Inf on the device.
     """
+    l0, l1 = _layer_range(layers, cache.dims.L)
     if not cache.host_resident:
-        geom = cache.geometry(hm)
-        pk, pv = _pools(cache, in_place)
+        d = cache.dims
+        pk, pv = _pools(cache, in_place, l0, l1)
+        geom = Geometry(l1 - l0, d.B * d.p, d.t, d.h, d.d, hm)
         engine = FusionEngine(geom, plan, pk.dtype, pk.device, path)
-        return [(engine.run(pk.reshape(-1), pv.reshape(-1), threshold, keep_samples=keep_samples), 0)]
+        return [(engine.run(pk.reshape(-1), pv.reshape(-1), threshold, keep_samples=keep_samples), l0)]
     d = cache.dims
     dev = cache.device
-    kd = torch.empty(d.shape, dtype=cache.dtype, device=dev)
-    vd = torch.empty(d.shape, dtype=cache.dtype, device=dev)
+    shape = (l1 - l0,) + tuple(d.shape[1:])
+    kd = torch.empty(shape, dtype=cache.dtype, device=dev)
+    vd = torch.empty(shape, dtype=cache.dtype, device=dev)
     compute = torch.cuda.current_stream(dev)
     copy = torch.cuda.Stream(dev)
     copy.wait_stream(compute)  # kd / vd allocated on the compute stream
-    chunks = _stream_chunks(d.L)
+    chunks = _stream_chunks(l1 - l0)
     ready = []
     with torch.cuda.stream(copy):
         for c0, c1 in chunks:
-            kd[c0:c1].copy_(cache.keys[c0:c1], non_blocking=True)
-            vd[c0:c1].copy_(cache.values[c0:c1], non_blocking=True)
+            kd[c0:c1].copy_(cache.keys[l0 + c0:l0 + c1], non_blocking=True)
+            vd[c0:c1].copy_(cache.values[l0 + c0:l0 + c1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
             ready.append(ev)
@@ -622,12 +641,12 @@ def _run_fusion(cache: PagedKvCache, plan: Plan, hm: int, threshold: float, in_p
             engines[nl] = FusionEngine(Geometry(nl, d.B * d.p, d.t, d.h, d.d, hm), plan, cache.dtype,
                                        dev, path)
         st = engines[nl].run(kc.reshape(-1), vc.reshape(-1), threshold, keep_samples=keep_samples)
-        out.append((st, c0))
+        out.append((st, l0 + c0))
     kd.record_stream(copy)
     vd.record_stream(copy)
     if int(bad.item()):
         raise InvalidCacheError("cache contains NaN or Inf entries")
-    if in_place:
+    if in_place and (l0, l1) == (0, d.L):
         cache.keys_dev, cache.values_dev = kd, vd
     return out
 
@@ -655,13 +674,16 @@ def _outcomes(runs, keep_samples, rows, bpr, shape, check: bool = True) -> list[
 
 def fuse_batch(cache: PagedKvCache, cfg: FusionConfig, *, in_place: bool = False,
                keep_samples: bool | None = None, path: int = N.PATH_AUTO,
-               audit: bool = True) -> list[FusionOutcome]:
+               audit: bool = True, layers=None) -> list[FusionOutcome]:
     """Batch Fast-Fusion across requests, all layers at once (fusion.py:360-374).
 
     Returns one outcome per layer (folded) or per (layer, kv head) in
     per-head mode, layer-major. ``audit`` runs the device table audit after
     fusion and raises CorruptionError on an inconsistent table, as the
-    reference does per layer (fusion.py:315).
+    reference does per layer (fusion.py:315). ``layers`` (a contiguous range,
+    e.g. ``dist.shard_units(L, world, rank)``) fuses only those layers -- layers
+    are independent (fusion.py:367-374), so a shard's outcomes equal the
+    full run's for the same layers; report.layer keeps the cache index.
     """
     if cfg.variant != "bff":
         raise ConfigError(f"fuse_batch requires variant 'bff', got {cfg.variant!r}")
@@ -670,14 +692,14 @@ def fuse_batch(cache: PagedKvCache, cfg: FusionConfig, *, in_place: bool = False
     geom = cache.geometry(hm)
     plan = bff_plan(dims.B, dims.p, cfg.group_size)
     ks = _want_samples(keep_samples, plan, geom.units)
-    runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path)
+    runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path, layers)
     shape = (dims.t, 1, dims.d) if hm else (dims.t, dims.h, dims.d)
     return _outcomes(runs, ks, dims.B, dims.p, shape, check=audit)
 
 
 def fuse_chunks(cache: PagedKvCache, cfg: FusionConfig, chunk_tokens: int, *,
                 in_place: bool = False, keep_samples: bool | None = None,
-                path: int = N.PATH_AUTO, audit: bool = True) -> list[FusionOutcome]:
+                path: int = N.PATH_AUTO, audit: bool = True, layers=None) -> list[FusionOutcome]:
     """Chunks Fast-Fusion across the chunks of each request (fusion.py:377-415).
 
     Rows are (request, chunk); trees never cross requests; physical blocks
@@ -691,7 +713,7 @@ def fuse_chunks(cache: PagedKvCache, cfg: FusionConfig, chunk_tokens: int, *,
     geom = cache.geometry(hm)
     plan = cff_plan(dims.B, C, bpc, cfg.group_size)
     ks = _want_samples(keep_samples, plan, geom.units)
-    runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path)
+    runs = _run_fusion(cache, plan, hm, cfg.threshold, in_place, ks, path, layers)
     shape = (dims.t, 1, dims.d) if hm else (dims.t, dims.h, dims.d)
     outcomes = _outcomes(runs, ks, dims.B * C, bpc, shape, check=audit)
     for oc in outcomes:  # reusable = {refcount > 1} (fusion.py:409-411)

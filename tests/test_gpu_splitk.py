@@ -47,7 +47,7 @@ def test_splitk_matches_unsplit(dtype, variant):
     for sa, sb in zip(a.level_stats, b.level_stats):
         assert torch.equal(sa[..., :4], sb[..., :4])  # counts
         n = sa[..., 3:4].clamp(min=1)  # moments per sample: fp32 sums regroup across splits
-        torch.testing.assert_close(sa[..., 4:6] / n, sb[..., 4:6] / n, rtol=0, atol=2e-6)
+        torch.testing.assert_close(sa[..., 4:6] / n, sb[..., 4:6] / n, rtol=0, atol=2e-5)
         # min / max: single samples, each within the tensor-core accumulation error (~1e-4)
         torch.testing.assert_close(sa[..., 6:], sb[..., 6:], rtol=0, atol=3e-4)
     for xa, xb in zip(a.level_samples, b.level_samples):
