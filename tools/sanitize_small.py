@@ -1,4 +1,7 @@
-"""Tiny bf16 fusion runs (folded + per-head, tcgen05 path) for compute-sanitizer."""
+"""Tiny runs of every kernel family for compute-sanitizer (memcheck / synccheck /
+racecheck / initcheck): bf16 folded + per-head fusion (exact mode, tcgen05),
+float32 fusion (hi/lo split operands + split-K), CFF, request-major and
+scheduled decode, chunked prefill."""
 import os
 import sys
 
@@ -8,10 +11,35 @@ import torch
 import paper_2601_03067_b200 as K
 from paper_2601_03067_b200.workload import synthetic_kv
 
+torch.cuda.set_device(0)
 for hm in ("folded", "per_head"):
     L, B, p, t, h, d = 1, 8, 64, 16, 8, 128
     Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=5)
     cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
     outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8, head_mode=hm), keep_samples=True)
     torch.cuda.synchronize()
-    print(hm, sum(o.report.blocks_before for o in outs) / sum(o.report.blocks_after for o in outs))
+    print("bf16", hm, sum(o.report.blocks_before for o in outs) / sum(o.report.blocks_after for o in outs))
+# float32: split operands, split-K (few long tiles)
+Kt, Vt = synthetic_kv(2, 8, 64, 16, 8, 128, dtype=torch.float32, seed=6)
+cache = K.PagedKvCache(K.CacheDims(B=8, p=64, t=16, h=8, d=128, L=2), Kt, Vt)
+outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8))
+print("f32", outs[0].fused.state.path_name, outs[0].report.compression_ratio)
+# CFF + chunked prefill over the fused context
+Kt, Vt = synthetic_kv(1, 2, 64, 16, 2, 128, dtype=torch.bfloat16, seed=7, variant="cff")
+cache = K.PagedKvCache(K.CacheDims(B=2, p=64, t=16, h=2, d=128, L=1), Kt, Vt)
+oc = K.fuse_chunks(cache, K.FusionConfig(threshold=0.8, variant="cff"), 256)[0]
+st = oc.fused.state
+q = torch.randn(2, 16 * 16, 8, 128, device="cuda", dtype=torch.bfloat16)
+try:
+    K.chunk_prefill(q, st, 0, 2, 64, 16, 3)
+except Exception as exc:  # shape limits of the prefill kernels are not the point here
+    print("prefill skipped:", str(exc)[:80])
+# decode: request-major and sharing-aware
+Kt, Vt = synthetic_kv(1, 16, 64, 16, 2, 128, dtype=torch.bfloat16, seed=8)
+cache = K.PagedKvCache(K.CacheDims(B=16, p=64, t=16, h=2, d=128, L=1), Kt, Vt)
+st = K.fuse_batch(cache, K.FusionConfig(threshold=0.8))[0].fused.state
+qd = torch.randn(16, 8, 128, device="cuda", dtype=torch.bfloat16)
+o1, _ = K.paged_decode(qd, st, 0, 16, 64)
+o2, _ = K.paged_decode(qd, st, 0, 16, 64, schedule=K.state_decode_schedule(st, 0, 16, 64))
+torch.cuda.synchronize()
+print("decode max diff", float((o1 - o2).abs().max()))
