@@ -30,6 +30,9 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+# the decode leg keeps the whole 32-layer fused cache resident (~132 GB) next to the
+# fusion engine that builds it: expandable segments avoid caching-allocator fragmentation
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 CONFIGS = {
     # configs[1]: the headline

@@ -13,6 +13,7 @@ height) instead of recursively.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -25,7 +26,8 @@ def grouped(indices: list[int], group_size: int | None) -> list[list[int]]:
     return [list(indices[i : i + group_size]) for i in range(0, len(indices), group_size)]
 
 
-TILE_BAND = 4  # tile rows per launch-order band (L2 reuse of operand tiles)
+# tile rows per launch-order band (L2 reuse of operand tiles); KVF_TILE_BAND overrides (A/B)
+TILE_BAND = int(os.environ.get("KVF_TILE_BAND", "4"))
 
 
 @dataclass(frozen=True)
