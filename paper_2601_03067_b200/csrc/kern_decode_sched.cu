@@ -70,7 +70,7 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
                     int64_t p_blocks, int Hq, float sm_scale, const int32_t* __restrict__ meta,
                     const int32_t* __restrict__ sphys, const float* __restrict__ sks,
                     const float* __restrict__ svs, const int32_t* __restrict__ n_items_p,
-                    int64_t cap, float* __restrict__ part) {
+                    int64_t cap, float* __restrict__ part, int head_minor) {
   static_assert(2 * IB <= 32, "slot metadata of two items must fit in one warp");
   static_assert(T == 16 || T == 32, "blocks of 16 or 32 tokens");
   static_assert(IB >= DNS - 1, "the copy lookahead may not pass the next item");
@@ -99,8 +99,14 @@ decode_sched_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_const
   const int64_t my_items = (total - gidx0 + NW - 1) / NW;
   const int rowbase = (int)(layer * g.NB);
 
-  // schedule row of work index gi (head-major sweep)
+  // schedule row of work index gi: head-major sweep, or (folded schedules) head-minor --
+  // the KV heads of one item run on adjacent warps, so a block's head slices are read
+  // together instead of in h separate sweeps
   auto row_of = [&](int64_t gi, int& kvh) {
+    if (head_minor) {
+      kvh = (int)(gi % g.h);
+      return gi / g.h;
+    }
     kvh = (int)(gi / n_items);
     return (g.head_mode ? (int64_t)kvh * cap : 0) + gi % n_items;
   };
@@ -564,9 +570,14 @@ cudaError_t decode_sched_t(const DecodeArgs& a, cudaStream_t s) {
   const int64_t grid = std::min<int64_t>((int64_t)n_sm * per_sm, (work_max + DW - 1) / DW);
   if (grid < 1) return cudaSuccess;
   const SchedView& v = *a.sched;
+  static const int env_minor = [] {  // KVF_SCHED_HEAD_MINOR: sweep order A/B
+    const char* e = getenv("KVF_SCHED_HEAD_MINOR");
+    return e ? atoi(e) : 0;
+  }();
+  const int head_minor = (!a.g.head_mode && env_minor) ? 1 : 0;
   kern<<<(unsigned)grid, DW * 32, smem, s>>>(km, vm, a.q, a.q_dtype, a.g, a.layer, a.B, a.p_blocks,
                                             a.Hq, (float)a.sm_scale, v.meta, v.phys, v.ks, v.vs,
-                                            v.n_items, v.cap, (float*)a.ws);
+                                            v.n_items, v.cap, (float*)a.ws, head_minor);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_decode_combine(a, nit, IB, s);

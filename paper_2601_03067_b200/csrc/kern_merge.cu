@@ -824,6 +824,72 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
 }
 
 namespace {
+// Long vectors (r > 16384: folded units of 32-token blocks, MHA-sized heads): CTA per
+// (absorber, K|V) in two passes over column chunks -- pass 1 the norm of the member
+// sum, pass 2 the sum again, scaled and written -- so registers stay bounded for any r.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+merge_long_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
+                  typename AccOf<T>::type* __restrict__ knorm,
+                  typename AccOf<T>::type* __restrict__ vnorm,
+                  const typename AccOf<T>::type* __restrict__ oknorm,
+                  const typename AccOf<T>::type* __restrict__ ovnorm, int32_t* ws,
+                  int64_t n_total, ItemSel sel) {
+  using A = typename AccOf<T>::type;
+  __shared__ A red[32];
+  const LevelWs W(ws, n_total);
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int64_t nch = g.r() / VEC;
+  const int64_t n_items = sel.n(*W.count);
+  for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+    const bool is_v = sel.is_v(it);
+    T* pool = is_v ? pool_v : pool_k;
+    A* norm = is_v ? vnorm : knorm;
+    const int64_t gid = W.list[sel.idx(it)];
+    const int64_t u = gid / g.NB, gb = u * g.NB;
+    const int32_t l = (int32_t)(gid % g.NB);
+    const int n = W.mcnt[gid], s0 = W.mstart[gid];
+    // every thread walks the same member order, so both passes sum identically
+    auto member_sum = [&](int64_t c, A (&y)[VEC]) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) y[e] = A(0);
+      for (int v = 0; v <= n; ++v) {
+        const int32_t id = v == 0 ? l : W.members[s0 + v - 1];
+        const A nv = norm[gb + id];
+        const A inv = nv > A(0) ? A(1) / nv : A(0);
+        A x[VEC];
+        VecIO<T, VEC>::load(pool + g.base(u, id) + g.off(c * VEC), x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) y[e] += x[e] * inv;
+      }
+    };
+    A ss = 0;
+    for (int64_t c = tid; c < nch; c += bd) {
+      A y[VEC];
+      member_sum(c, y);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) ss += y[e] * y[e];
+    }
+    const A nrm = sqrt(block_sum(ss, red));
+    const A home = (is_v ? ovnorm : oknorm)[gid];
+    const A sc = nrm > A(0) ? (home > A(0) ? home : A(1)) / nrm : A(0);
+    // pass 2 reads the absorber's own chunk before overwriting it (same thread, same c)
+    A rs = 0;
+    for (int64_t c = tid; c < nch; c += bd) {
+      A y[VEC], rd[VEC];
+      member_sum(c, y);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) y[e] *= sc;
+      VecIO<T, VEC>::store(pool + g.base(u, l) + g.off(c * VEC), y, rd);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) rs += rd[e] * rd[e];
+    }
+    const A nn = sqrt(block_sum(rs, red));
+    if (tid == 0) norm[gid] = nn;
+    __syncthreads();
+  }
+}
+
 template <typename T, int VEC>
 cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
                       const void* ovn, int32_t* ws, int64_t n_total, ItemSel sel, cudaStream_t s) {
@@ -831,7 +897,12 @@ cudaError_t merge_reg(void* pk, void* pv, const Geom& g, void* kn, void* vn, con
   const int64_t nch = g.r() / VEC;
   int bd = 512;
   while (bd > 64 && (int64_t)(bd / 2) * (32 / VEC) >= nch) bd /= 2;
-  if (nch > (int64_t)bd * (32 / VEC)) return cudaErrorInvalidValue;
+  if (nch > (int64_t)bd * (32 / VEC)) {  // beyond the register-resident path
+    merge_long_kernel<T, VEC><<<dim3(148 * 4), 256, 0, s>>>((T*)pk, (T*)pv, g, (A*)kn, (A*)vn,
+                                                           (const A*)okn, (const A*)ovn, ws, n_total,
+                                                           sel);
+    return cudaGetLastError();
+  }
   dim3 grid(148 * 4, sel.which == 3 ? 2 : 1);
   merge_reg_kernel<T, VEC><<<grid, bd, 0, s>>>((T*)pk, (T*)pv, g, (A*)kn, (A*)vn, (const A*)okn,
                                                (const A*)ovn, ws, n_total, sel);

@@ -221,10 +221,9 @@ int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t N
   if (!valid_dtype(dtype)) return fail(KVF_ERR_INVALID, "bad dtype %d", dtype);
   if (!pool_k || !pool_v || !knorm || !vnorm || !orig_knorm || !orig_vnorm || !level_ws)
     return fail(KVF_ERR_INVALID, "null pointer");
-  const int64_t r = g.r();
-  if (r > 16384)
-    return fail(KVF_ERR_INVALID, "block vector length %lld exceeds the merge kernel's 16384",
-                (long long)r);
+  if (shadow && g.r() > 16384)
+    return fail(KVF_ERR_INVALID, "exact mode supports block vectors up to 16384 elements, got %lld",
+                (long long)g.r());
   if (which < 1 || which > 3) return fail(KVF_ERR_INVALID, "which must be 1 (K), 2 (V) or 3 (K and V)");
   if (shadow) {
     if (dtype != BF16) return fail(KVF_ERR_INVALID, "exact mode (shadow rows) is for bfloat16 pools");

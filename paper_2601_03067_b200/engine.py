@@ -200,7 +200,7 @@ class FusionEngine:
         self.filter_mode = path == N.PATH_TC and dtype == torch.float32
         # exact mode (bf16 pools): fp32 shadow rows of the fused key directions, so
         # re-scored decisions at levels >= 2 follow the reference's float64 directions
-        if exact is None:
+        if exact is None:  # exact mode covers r <= 16384; longer vectors merge on merge_long_kernel
             exact = path == N.PATH_TC and dtype == torch.bfloat16 and geom.r <= 16384 and geom.d % 8 == 0
         if exact and not (path == N.PATH_TC and dtype == torch.bfloat16):
             exact = False  # float32 / float64 pools keep fused keys at full precision already

@@ -252,3 +252,22 @@ def test_edge_cases_bf16_vs_oracle(case, head_mode):
             for ev in oc.report.fused_events:
                 assert tuple(ev.absorber) not in zero
                 assert all(tuple(s) not in zero for s in ev.absorbed)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["f32", "bf16"])
+def test_long_vectors_vs_oracle(dtype):
+    """Folded units longer than 16384 elements (32-token blocks, 8 heads, d = 128:
+    r = 32768) merge on the two-pass chunked kernel; bf16 runs without exact mode
+    there (shadow rows are capped at 16384), so its levels >= 2 use the stored-block
+    band (eps 1e-3, flips counted), float32 stays exact."""
+    L, B, p, t, h, d = 1, 8, 8, 32, 8, 128
+    cache, Kh, Vh = _cache(L, B, p, t, h, d, dtype, seed=61)
+    outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8), keep_samples=True)
+    st = outs[0].fused.state
+    assert st.geom.r == 32768 and st.exact == (dtype == torch.float32)
+    eps = 1e-9 if dtype == torch.float32 else 1e-3
+    ref = O.fuse_unit(O.layer_unit(Kh, 0), O.layer_unit(Vh, 0), B, p, 0.8,
+                      gpu_absorber=st.absorber[0].cpu().numpy(), eps=eps)
+    _compare_unit(outs[0], ref, dtype)
+    if dtype == torch.float32:
+        assert ref.flips == 0
