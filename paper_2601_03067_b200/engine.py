@@ -283,12 +283,18 @@ class FusionEngine:
             raise ConfigError("gathered compaction needs folded units")
         self.compact_mode = compact_mode
         self.staged = None
+        self.stage_units = U
         if compact_from is not None:
             self.live = torch.empty((U, NB), dtype=torch.int32, device=dev)
             self.rank = torch.empty((U, NB + 1), dtype=torch.int32, device=dev)
             self.acount = torch.empty(U, dtype=torch.int32, device=dev)
             if compact_mode == "staged":
-                self.staged = torch.empty(U * NB * geom.r, dtype=torch.bfloat16, device=dev)
+                # staging holds the alive K rows of `stage_units` units at a time (compacted
+                # levels run in unit chunks): ~STAGE_BUDGET instead of a second full K pool
+                per_unit = NB * geom.r * 2
+                self.stage_units = max(1, min(U, STAGE_BUDGET // max(per_unit, 1)))
+                self.staged = torch.empty(self.stage_units * NB * geom.r, dtype=torch.bfloat16,
+                                          device=dev)
 
     def capture(self, pool_k: torch.Tensor, pool_v: torch.Tensor, threshold: float, *,
                 keep_samples: bool = False) -> "CapturedFusion":
@@ -365,42 +371,50 @@ class FusionEngine:
                 samples = torch.empty((U, max(lv["rect_total"], 1)), dtype=torch.float64, device=dev)
                 samples.view(torch.int64).fill_(-1)  # all-ones bit pattern = NaN
             compact = self.compact_from is not None and self.plan.levels[li].height >= self.compact_from
-            if compact:
-                N.call("kvf_alive_rank", 0, U, NB, N.ptr(alive_t), N.ptr(self.live), N.ptr(self.rank),
-                       N.ptr(self.acount), sp)
-                launches += 1
-                if self.staged is not None:
-                    N.call("kvf_stage_rows", N.ptr(opnd), N.DT_BF16, *g.args(), 0, U, N.ptr(self.live),
-                           N.ptr(self.acount), N.ptr(self.staged), sp)
-                    launches += 1
-            if time_sim:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
+            # compacted levels run in unit chunks that fit the staging buffer
+            cu = self.stage_units if compact and self.staged is not None else U
             # re-score band: the fp32 accumulation error at level 1 of a bf16 pool, plus the
             # bf16 rounding of the operands where the tensor cores read rounded copies
             wide = self.exact and self.plan.levels[li].height >= 2
             band = (RESCORE_BAND_WIDE if wide else RESCORE_BAND) if self.rescore_cap else 0.0
-            N.call(
-                "kvf_similarity_select", N.ptr(pool_k), dt, *g.args(), 0, U, N.ptr(knorm),
-                N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber), N.ptr(lv["merges"]), nm,
-                N.ptr(lv["tiles"]), nt, float(threshold), N.ptr(self.partials), N.ptr(samples),
-                N.ptr(lv["sample_off"]) if samples is not None else None,
-                samples.shape[1] if samples is not None else 0,
-                N.ptr(self.live) if compact else None, N.ptr(self.rank) if compact else None,
-                N.ptr(self.staged) if compact and self.staged is not None else None,
-                N.ptr(self.rescore), self.rescore_cap, band,
-                N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx),
-                self.nsplit[li], N.ptr(self.split_part) if self.nsplit[li] > 1 else None,
-                N.ptr(self.split_count) if self.nsplit[li] > 1 else None, self.path, sp,
-            )
-            if self.rescore_cap:
-                launches += 1
-                # pairs within RESCORE_BAND of the threshold at this level (decided in float64)
-                st.near_threshold.append(self.rescore[4 * self.rescore_cap:4 * self.rescore_cap + 1].clone())
-            if time_sim:
-                e1.record(stream)
-                st.sim_events.append((e0, e1, li))
+            for u0 in range(0, U, cu):
+                nU = min(cu, U - u0)
+                if compact:
+                    N.call("kvf_alive_rank", u0, nU, NB, N.ptr(alive_t), N.ptr(self.live),
+                           N.ptr(self.rank), N.ptr(self.acount), sp)
+                    launches += 1
+                    if self.staged is not None:
+                        N.call("kvf_stage_rows", N.ptr(opnd), N.DT_BF16, *g.args(), u0, nU,
+                               N.ptr(self.live), N.ptr(self.acount), N.ptr(self.staged), sp)
+                        launches += 1
+                if time_sim:  # the similarity launch (+ its re-score) only, per chunk
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                N.call(
+                    "kvf_similarity_select", N.ptr(pool_k), dt, *g.args(), u0, nU, N.ptr(knorm),
+                    N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber), N.ptr(lv["merges"]), nm,
+                    # partials are packed per level: unit stride nt * ppt slots of 5 doubles
+                    N.ptr(lv["tiles"]), nt, float(threshold),
+                    N.ptr(self.partials.view(-1)[u0 * nt * self.ppt * 5:]),
+                    N.ptr(samples[u0:]) if samples is not None else None,
+                    N.ptr(lv["sample_off"]) if samples is not None else None,
+                    samples.shape[1] if samples is not None else 0,
+                    N.ptr(self.live) if compact else None, N.ptr(self.rank) if compact else None,
+                    N.ptr(self.staged) if compact and self.staged is not None else None,
+                    N.ptr(self.rescore), self.rescore_cap, band,
+                    N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx),
+                    self.nsplit[li], N.ptr(self.split_part) if self.nsplit[li] > 1 else None,
+                    N.ptr(self.split_count) if self.nsplit[li] > 1 else None, self.path, sp,
+                )
+                if self.rescore_cap:
+                    launches += 1
+                    # pairs within the band of the threshold in this launch (decided in float64)
+                    st.near_threshold.append(
+                        self.rescore[4 * self.rescore_cap:4 * self.rescore_cap + 1].clone())
+                if time_sim:
+                    e1.record(stream)
+                    st.sim_events.append((e0, e1, li))
             N.call(
                 "kvf_level_stats", 0, U, U, NB, N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber),
                 N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt,
@@ -441,6 +455,7 @@ class FusionEngine:
 
 COMPACT_BIG_MERGE = 65536  # blocks per merge (left + right)
 SPLIT_PART_BUDGET = 512 << 20  # bytes of split-K partials per engine
+STAGE_BUDGET = 4 << 30  # bytes of staged alive K rows (compacted levels, unit chunks)
 _TILE_PART_BYTES = 256 * 256 * 4  # one CTA pair's fp32 accumulator tile
 
 
