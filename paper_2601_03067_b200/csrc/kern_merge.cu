@@ -676,13 +676,14 @@ merge_warp_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
 struct RingSlotMeta {
   float inv, home;
   int32_t gid, flags;  // flags: bit0 last vector of the item, bit1 V tensor
+  int32_t sh, ash;     // exact mode, keys: the vector's / the absorber's shadow row (-1: none)
 };
 template <int CPL, int NS>
 __global__ void __launch_bounds__(256, 2)
 merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict__ pool_v, Geom g,
                   float* __restrict__ knorm, float* __restrict__ vnorm,
                   const float* __restrict__ oknorm, const float* __restrict__ ovnorm,
-                  int32_t* ws, int64_t n_total, ItemSel sel) {
+                  int32_t* ws, int64_t n_total, ItemSel sel, ExactArgs ex) {
   constexpr int VB = CPL * 512;  // vector bytes (32 lanes x CPL x 16 B)
   extern __shared__ __align__(128) uint8_t rsm[];
   const LevelWs W(ws, n_total);
@@ -705,7 +706,7 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
   int64_t it_i = gw;
   int v_i = 0, n_i = 0, s0_i = 0;
   int64_t gid_i = 0;
-  int32_t id_l = 0;
+  int32_t id_l = 0, sh_l = -1, ash_i = -1;
   float inv_l = 0.f, home_i = 0.f;
   auto load_item = [&]() {  // all lanes
     if (it_i >= n_items) return;
@@ -718,26 +719,35 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
     const int64_t gb = (gid_i / g.NB) * g.NB;
     id_l = (int32_t)(gid_i - gb);
     inv_l = 0.f;
+    sh_l = -1;
     if (lane <= n_i) {
       if (lane > 0) id_l = W.members[s0_i + lane - 1];
       const float nv = norm[gb + id_l];
       inv_l = nv > 0.f ? 1.f / nv : 0.f;
+      if (ex.shadow && !is_v) {
+        sh_l = ex.sidx[gb + id_l];
+        if (sh_l >= 0) inv_l = 1.f;  // shadow rows are unit directions
+      }
     }
+    ash_i = __shfl_sync(0xffffffffu, sh_l, 0);
   };
   uint32_t q_i = 0, q_c = 0;
   auto issue = [&]() {  // all lanes
     if (it_i >= n_items) return;
     const bool is_v = sel.is_v(it_i);
-    int32_t id;
+    int32_t id, sh;
     float inv;
     if (v_i < 32) {
       id = __shfl_sync(0xffffffffu, id_l, v_i);
       inv = __shfl_sync(0xffffffffu, inv_l, v_i);
+      sh = __shfl_sync(0xffffffffu, sh_l, v_i);
     } else {  // groups beyond one warp of members
       const int64_t gb = (gid_i / g.NB) * g.NB;
       id = W.members[s0_i + v_i - 1];
       const float nv = (is_v ? vnorm : knorm)[gb + id];
       inv = nv > 0.f ? 1.f / nv : 0.f;
+      sh = (ex.shadow && !is_v) ? ex.sidx[gb + id] : -1;
+      if (sh >= 0) inv = 1.f;
     }
     const int s = q_i % NS;
     const int64_t u = gid_i / g.NB;
@@ -747,11 +757,16 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
       m.home = home_i;
       m.gid = (int32_t)gid_i;
       m.flags = (v_i == n_i ? 1 : 0) | (is_v ? 2 : 0);
+      m.sh = sh;
+      m.ash = ash_i;
       smeta[s] = m;
-      mbar_expect_tx(&bars[s], (uint32_t)VB);  // release: slot meta visible after the wait
+      if (sh >= 0)
+        mbar_arrive(&bars[s]);  // shadow row: the consumer reads it from global memory
+      else
+        mbar_expect_tx(&bars[s], (uint32_t)VB);  // release: slot meta visible after the wait
     }
     __syncwarp();
-    if (lane < g.t) {
+    if (sh < 0 && lane < g.t) {
       const __nv_bfloat16* src = (is_v ? pool_v : pool_k) + g.base(u, id) + lane * rstride;
       bulk_g2s(ring + (size_t)s * VB + lane * segb, src, segb, &bars[s]);
     }
@@ -776,15 +791,26 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
     mbar_wait(&bars[s], (q_c / NS) & 1);
     const RingSlotMeta m = smeta[s];
     const uint4* sp = reinterpret_cast<const uint4*>(ring + (size_t)s * VB);
+    if (m.sh >= 0) {  // exact mode: fused key member, its fp32 unit direction
+      const float* row = ex.shadow + (int64_t)m.sh * g.r();
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const uint4 raw = sp[q * 32 + lane];
-      const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+      for (int q = 0; q < CPL; ++q) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(row + (q * 32 + lane) * 8));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(row + (q * 32 + lane) * 8 + 4));
+        acc[q][0] += a.x; acc[q][1] += a.y; acc[q][2] += a.z; acc[q][3] += a.w;
+        acc[q][4] += b.x; acc[q][5] += b.y; acc[q][6] += b.z; acc[q][7] += b.w;
+      }
+    } else {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(p2[e]);
-        acc[q][2 * e] = fmaf(f.x, m.inv, acc[q][2 * e]);
-        acc[q][2 * e + 1] = fmaf(f.y, m.inv, acc[q][2 * e + 1]);
+      for (int q = 0; q < CPL; ++q) {
+        const uint4 raw = sp[q * 32 + lane];
+        const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(p2[e]);
+          acc[q][2 * e] = fmaf(f.x, m.inv, acc[q][2 * e]);
+          acc[q][2 * e + 1] = fmaf(f.y, m.inv, acc[q][2 * e + 1]);
+        }
       }
     }
     __syncwarp();  // the slot may be refilled by the next issue
@@ -804,10 +830,32 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
     const int64_t u = m.gid / g.NB;
     const int32_t l = (int32_t)(m.gid % g.NB);
     __nv_bfloat16* xl = pool + g.base(u, l);
+    // exact mode, keys: the absorber's shadow row (taken on its first fusion)
+    float* srow = nullptr;
+    const float inv_n = nrm > 0.f ? 1.f / nrm : 0.f;
+    if (ex.shadow && !is_v) {
+      int sl = m.ash;
+      if (sl < 0) {
+        if (lane == 0) {
+          sl = atomicAdd(ex.scount, 1);
+          if (sl < ex.cap) ex.sidx[m.gid] = sl;
+        }
+        sl = __shfl_sync(0xffffffffu, sl, 0);
+        if (sl >= ex.cap) sl = -1;
+      }
+      if (sl >= 0) srow = ex.shadow + (int64_t)sl * g.r();
+    }
     float rs = 0.f;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       float yv[8], rd[8];
+      if (srow) {
+        float* d8 = srow + (q * 32 + lane) * 8;
+        *reinterpret_cast<float4*>(d8) = make_float4(acc[q][0] * inv_n, acc[q][1] * inv_n,
+                                                     acc[q][2] * inv_n, acc[q][3] * inv_n);
+        *reinterpret_cast<float4*>(d8 + 4) = make_float4(acc[q][4] * inv_n, acc[q][5] * inv_n,
+                                                         acc[q][6] * inv_n, acc[q][7] * inv_n);
+      }
 #pragma unroll
       for (int e = 0; e < 8; ++e) yv[e] = acc[q][e] * sc;
       VecIO<__nv_bfloat16, 8>::store(xl + g.off((int64_t)(q * 32 + lane) * 8), yv, rd);
@@ -961,9 +1009,12 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
   const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;
+  const bool ring_ok = std::is_same<T, __nv_bfloat16>::value && g.head_mode &&
+                       (vbytes == 4096 || vbytes == 2048) && g.t <= 32 && (g.d * 2) % 16 == 0 &&
+                       can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g) && !getenv("KVF_MERGE_NO_RING");
   if (ex.shadow) {  // exact mode (bf16 pools, keys)
     if (!std::is_same<T, __nv_bfloat16>::value) return cudaErrorInvalidValue;
-    if (!(tma_ok && !g.head_mode && (sel.which & 1))) {
+    if (!(((tma_ok && !g.head_mode) || ring_ok) && (sel.which & 1))) {
       // keys on the float64 CTA-per-absorber kernel, values below on the usual path
       if (sel.which & 1) {
         cudaError_t e = launch_exact_merge_keys(pk, g, (float*)kn, (const float*)okn, ex.shadow, ex.cap,
@@ -975,7 +1026,7 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
     }
   }
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-    if (ex.shadow) {  // folded exact mode: keys and values in one ring pass
+    if (ex.shadow && !g.head_mode) {  // folded exact mode: keys and values in one ring pass
       const int64_t ept = (r + MG_CONSUMERS - 1) / MG_CONSUMERS;
       if (ept <= 8)
         return merge_tma<T, 8>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
@@ -986,15 +1037,14 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
       return merge_tma<T, 64>(pk, pv, g, kn, vn, okn, ovn, ws, n_total, nbuf, slot_bytes, sel, ex, s);
     }
     // per-head units of 2 or 4 KB: warp per item, per-warp smem ring (3 slots)
-    if (g.head_mode && (vbytes == 4096 || vbytes == 2048) && g.t <= 32 && (g.d * 2) % 16 == 0 &&
-        can_vectorize<T>(pk, g) && can_vectorize<T>(pv, g) && !getenv("KVF_MERGE_NO_RING")) {
+    if (ring_ok) {
       auto go = [&](auto kern, int ns, int wpb, int per_sm) {
         const int smem = wpb * ns * (int)vbytes + wpb * ns * (8 + (int)sizeof(RingSlotMeta));
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         kern<<<148 * per_sm, wpb * 32, smem, s>>>((__nv_bfloat16*)pk, (__nv_bfloat16*)pv, g, (float*)kn,
                                                   (float*)vn, (const float*)okn, (const float*)ovn, ws,
-                                                  n_total, sel);
+                                                  n_total, sel, ex);
         return cudaGetLastError();
       };
       // measured (cfg2 per-head, 2 steps): 8 warps x 3 slots x 2 CTAs/SM 23.6 ms; 6 x 4 x 2 28.6;
