@@ -55,6 +55,11 @@ struct Geom {
     if (!head_mode) return k;
     return (k / d) * ((int64_t)h * d) + (k % d);
   }
+  // the same in 32-bit arithmetic (k < r <= INT32_MAX)
+  __host__ __device__ int32_t off32(int32_t k) const {
+    if (!head_mode) return k;
+    return (k / d) * (h * d) + (k % d);
+  }
 };
 
 template <typename T>

@@ -182,7 +182,8 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_tot
                                const int32_t* tile_off, int nt, const double* partials,
                                double* stats, int32_t* level_ws, cudaStream_t s) {
   LevelWs W(level_ws, n_total);
-  cudaError_t e = cudaMemsetAsync(W.count, 0, 2 * sizeof(int32_t), s);  // count, cursor
+  // count, cursor, merge item fetch counter
+  cudaError_t e = cudaMemsetAsync(W.count, 0, 3 * sizeof(int32_t), s);
   if (e != cudaSuccess || nm == 0 || nU == 0) return e;
   dim3 grid(nm, (unsigned)nU);
   level_stats_kernel<<<grid, LS_THREADS, 0, s>>>(u0, NB, n_total, fusable, alive, absorber,
@@ -257,9 +258,11 @@ struct SlotMeta {
   float inv;   // 1 / stored norm of the vector in the slot (0 for zero vectors)
   float home;  // item: original norm of the absorber's home slot
   int32_t gid; // item: global absorber id u * NB + l
-  int32_t flags;  // bit0: last vector of the item, bit1: V tensor
-  int32_t sh;  // exact mode, keys: shadow row of this vector (no bulk copy) or -1
+  int32_t flags;  // bit0: last slot of the item, bit1: V tensor, bit2: end of the work
+  int32_t sh;  // exact mode, keys: shadow row of this vector or -1
   int32_t ash; // exact mode, keys: the absorber's shadow row (-1: none yet)
+  int32_t half;  // 0: the slot holds a pool vector; 1 / 2: first / second half of the
+                 // fp32 shadow row sh (ring-fed shadow rows); -1: consumers read row sh
 };
 
 // Exact-decision mode (kern_exact.cu): fused key directions live as fp32 shadow
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(MG_THREADS, 2)
 merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* __restrict__ knorm,
                  float* __restrict__ vnorm, const float* __restrict__ oknorm,
                  const float* __restrict__ ovnorm, int32_t* ws, int64_t n_total, int nbuf,
-                 int slot_bytes, ItemSel sel, ExactArgs ex) {
+                 int slot_bytes, ItemSel sel, ExactArgs ex, int ring_shadow) {
   constexpr int VEC = 16 / (int)sizeof(T);
   constexpr int CPT = EPT / VEC;  // 16-byte chunks per consumer thread
   extern __shared__ __align__(128) uint8_t msm[];
@@ -285,8 +288,12 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)nbuf * slot_bytes);
   uint64_t* empty = full + MG_MAX_BUF;
   SlotMeta* meta = reinterpret_cast<SlotMeta*>(empty + MG_MAX_BUF);
+  // per-item reductions, double-buffered by item parity so each needs one barrier:
+  // red[2][8] norm of the member sum, red2[2][8] stored norm (written by consumer 0 of
+  // the next item, after that item's barrier), slot_bc[2] the absorber's shadow row
   float* red = reinterpret_cast<float*>(meta + MG_MAX_BUF);
-  int* slot_bc = reinterpret_cast<int*>(red + 16);
+  float* red2 = red + 16;
+  int* slot_bc = reinterpret_cast<int*>(red2 + 16);
   const LevelWs W(ws, n_total);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t r = g.r();
@@ -339,18 +346,50 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       }
       return x;
     };
+    // items are fetched dynamically (item sizes vary with the member count); every
+    // producer's last fetch is the one past the end, and the numerically last of
+    // those resets the counter for the next launch
+    auto fetch = [&]() {
+      int v = 0;
+      if (lane == 0) {
+        v = atomicAdd(W.fetch, 1);
+        if (v == n_items + (int)gridDim.x - 1) atomicExch(W.fetch, 0);
+      }
+      return __shfl_sync(0xffffffffu, v, 0);
+    };
+    // one slot: wait for it, publish the metadata, start its copy (or just arrive)
+    auto put = [&](uint32_t qq, const SlotMeta& mt, const void* src, uint32_t bytes, bool rows) {
+      const int s = qq % nbuf;
+      mbar_wait(&empty[s], ((qq / nbuf) & 1) ^ 1);
+      meta[s] = mt;
+      if (src == nullptr) {
+        mbar_arrive(&full[s]);
+        return;
+      }
+      mbar_expect_tx(&full[s], bytes);  // release: meta visible after the wait
+      uint8_t* dst = ring + (size_t)s * slot_bytes;
+      if (!rows) {
+        bulk_g2s(dst, src, bytes, &full[s]);
+      } else {  // per-head pool vector: one bulk copy per token row
+        const uint32_t segb = (uint32_t)(g.d * sizeof(T));
+        for (int tk = 0; tk < g.t; ++tk)
+          bulk_g2s(dst + tk * segb, reinterpret_cast<const T*>(src) + (int64_t)tk * g.h * g.d, segb,
+                   &full[s]);
+      }
+    };
     uint32_t q = 0;
-    int it = blockIdx.x;
+    int it = fetch();
     Item cur = load_item(it);
     while (cur.valid) {
-      const Item nxt = load_item(it + gridDim.x);
+      const int it_next = fetch();
+      const Item nxt = load_item(it_next);
       const bool is_v = sel.is_v(it);
       const T* pool = is_v ? pool_v : pool_k;
       const int64_t u = cur.gid / g.NB;
       const int64_t gb = u * g.NB;
       const int s0 = W.mstart[cur.gid];
       const int32_t ash = __shfl_sync(0xffffffffu, cur.sh, 0);
-      for (int v = 0; v <= cur.n; ++v, ++q) {
+      for (int v = 0; v <= cur.n; ++v) {
         int32_t id, sh;
         float inv;
         if (v < 32) {
@@ -364,57 +403,97 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
           sh = (ex.shadow && !is_v) ? ex.sidx[gb + id] : -1;
           if (sh >= 0) inv = 1.f;
         }
-        if (lane == 0) {
-          const int s = q % nbuf;
-          mbar_wait(&empty[s], ((q / nbuf) & 1) ^ 1);
-          SlotMeta mt;
-          mt.inv = inv;
-          mt.home = cur.home;
-          mt.gid = cur.gid;
-          mt.flags = (v == cur.n ? 1 : 0) | (is_v ? 2 : 0);
-          mt.sh = sh;
-          mt.ash = ash;
-          meta[s] = mt;
-          if (sh >= 0) {  // consumers read the shadow row from global memory
-            mbar_arrive(&full[s]);
-          } else {
-            mbar_expect_tx(&full[s], vbytes);  // release: meta visible after the wait
-            const T* src = pool + g.base(u, id);
-            uint8_t* dst = ring + (size_t)s * slot_bytes;
-            if (!g.head_mode) {
-              bulk_g2s(dst, src, vbytes, &full[s]);
-            } else {
-              const uint32_t segb = (uint32_t)(g.d * sizeof(T));
-              for (int tk = 0; tk < g.t; ++tk)
-                bulk_g2s(dst + tk * segb, src + (int64_t)tk * g.h * g.d, segb, &full[s]);
-            }
+        SlotMeta mt;
+        mt.inv = inv;
+        mt.home = cur.home;
+        mt.gid = cur.gid;
+        mt.flags = (v == cur.n ? 1 : 0) | (is_v ? 2 : 0);
+        mt.sh = sh;
+        mt.ash = ash;
+        if (sh >= 0 && ring_shadow) {  // fp32 shadow row: two slots of r / 2 floats
+          const float* row = ex.shadow + (int64_t)sh * r;
+          const uint32_t hb = (uint32_t)(r / 2 * sizeof(float));
+          if (lane == 0) {
+            SlotMeta m1 = mt;
+            m1.flags &= ~1;
+            m1.half = 1;
+            put(q, m1, row, hb, false);
+            mt.half = 2;
+            put(q + 1, mt, row + r / 2, hb, false);
           }
+          q += 2;
+        } else {
+          mt.half = sh >= 0 ? -1 : 0;
+          if (lane == 0)
+            put(q, mt, sh >= 0 ? nullptr : (const void*)(pool + g.base(u, id)), vbytes, g.head_mode != 0);
+          q += 1;
         }
       }
       cur = nxt;
-      it += gridDim.x;
+      it = it_next;
+    }
+    if (lane == 0) {  // end of the work for this CTA's consumers
+      SlotMeta mt;
+      mt.flags = 4;
+      mt.half = 0;
+      mt.sh = -1;
+      put(q, mt, nullptr, 0, false);
     }
     return;
   }
   // consumers: everything per vector comes from the slot (data + meta)
   const int ct = threadIdx.x - 32;
-  const int64_t nch = r / VEC;
+  const int nch = (int)(r / VEC);
+  const int nch_h = nch / 2;  // 16-byte chunks of T in the first half of a vector
   uint32_t q = 0;
   float acc[EPT];
 #pragma unroll
   for (int e = 0; e < EPT; ++e) acc[e] = 0.f;
-  for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+  const int cw = ct >> 5;
+  int par = 0;
+  float* prev_norm = nullptr;  // consumer 0: where the previous item's stored norm goes
+  auto finish_prev = [&](int pp) {  // after a barrier: every warp's partial is in red2[pp]
+    if (ct == 0 && prev_norm) {
+      float t = 0.f;
+#pragma unroll
+      for (int w = 0; w < MG_CONSUMERS / 32; ++w) t += red2[pp * 8 + w];
+      *prev_norm = sqrtf(t);
+    }
+  };
+  for (;;) {
     SlotMeta mt;
+    bool done = false;
     for (;;) {
       const int s = q % nbuf;
       mbar_wait(&full[s], (q / nbuf) & 1);
       mt = meta[s];
+      if (mt.flags & 4) {
+        done = true;
+        break;
+      }
       const T* sp = reinterpret_cast<const T*>(ring + (size_t)s * slot_bytes);
-      if (mt.sh >= 0) {  // exact mode: fused member, its fp32 unit direction
+      if (mt.half > 0) {  // exact mode: half of a fused member's fp32 unit direction
+        const float* hs = reinterpret_cast<const float*>(ring + (size_t)s * slot_bytes);
+        const int c_lo = mt.half == 1 ? 0 : nch_h, c_hi = mt.half == 1 ? nch_h : nch;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+          const int c = ct + k * MG_CONSUMERS;
+          if (c >= c_lo && c < c_hi) {
+#pragma unroll
+            for (int e4 = 0; e4 < VEC; e4 += 4) {
+              const float4 f = *reinterpret_cast<const float4*>(hs + (c - c_lo) * VEC + e4);
+              acc[k * VEC + e4 + 0] += f.x;
+              acc[k * VEC + e4 + 1] += f.y;
+              acc[k * VEC + e4 + 2] += f.z;
+              acc[k * VEC + e4 + 3] += f.w;
+            }
+          }
+        }
+      } else if (mt.sh >= 0) {  // exact mode: fused member, its fp32 unit direction
         const float* row = ex.shadow + (int64_t)mt.sh * r;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-          const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+          const int c = ct + k * MG_CONSUMERS;
           if (c < nch) {
 #pragma unroll
             for (int e4 = 0; e4 < VEC; e4 += 4) {
@@ -429,7 +508,7 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       } else {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-          const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+          const int c = ct + k * MG_CONSUMERS;
           if (c < nch) {
             float x[VEC];
             VecIO<T, VEC>::load(sp + c * VEC, x);
@@ -443,38 +522,51 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
       ++q;
       if (mt.flags & 1) break;
     }
+    if (done) {
+      asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+      finish_prev(par ^ 1);
+      break;
+    }
     const bool is_v = mt.flags & 2;
     T* pool = is_v ? pool_v : pool_k;
     float* norm = is_v ? vnorm : knorm;
     const int64_t u = mt.gid / g.NB;
     const int32_t l = (int32_t)(mt.gid % g.NB);
+    // exact mode, keys: the absorber's shadow row (taken on its first fusion); published
+    // through the norm reduction's barriers (every consumer reads it before the next
+    // item's reduction, the only place it is written again)
+    const bool want_row = ex.shadow && !is_v;
+    if (want_row && ct == 0) {
+      int sl = mt.ash;
+      if (sl < 0) {
+        sl = atomicAdd(ex.scount, 1);
+        if (sl < ex.cap) ex.sidx[mt.gid] = sl; else sl = -1;
+      }
+      slot_bc[par] = sl;
+    }
     float ss = 0.f;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) ss = fmaf(acc[e], acc[e], ss);
-    const float nrm = sqrtf(consumer_sum(ss, red));
+    ss = warp_sum(ss);
+    if (lane == 0) red[par * 8 + cw] = ss;
+    asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+    finish_prev(par ^ 1);
+    float nsum = 0.f;
+#pragma unroll
+    for (int w = 0; w < MG_CONSUMERS / 32; ++w) nsum += red[par * 8 + w];
+    const float nrm = sqrtf(nsum);
     const float sc = nrm > 0.f ? (mt.home > 0.f ? mt.home : 1.f) / nrm : 0.f;
     T* xl = pool + g.base(u, l);
-    // exact mode, keys: the absorber's shadow row (taken on its first fusion)
     float* srow = nullptr;
     const float inv_n = nrm > 0.f ? 1.f / nrm : 0.f;
-    if (ex.shadow && !is_v) {
-      if (ct == 0) {
-        int sl = mt.ash;
-        if (sl < 0) {
-          sl = atomicAdd(ex.scount, 1);
-          if (sl < ex.cap) ex.sidx[mt.gid] = sl; else sl = -1;
-        }
-        *slot_bc = sl;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
-      const int sl = *slot_bc;
-      asm volatile("bar.sync 1, %0;" ::"n"(MG_CONSUMERS) : "memory");
+    if (want_row) {
+      const int sl = slot_bc[par];
       if (sl >= 0) srow = ex.shadow + (int64_t)sl * r;
     }
     float rs = 0.f;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
-      const int64_t c = ct + (int64_t)k * MG_CONSUMERS;
+      const int c = ct + k * MG_CONSUMERS;
       if (c < nch) {
         float y[VEC], rd[VEC];
         if (srow) {
@@ -486,15 +578,17 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
         }
 #pragma unroll
         for (int e = 0; e < VEC; ++e) y[e] = acc[k * VEC + e] * sc;
-        VecIO<T, VEC>::store(xl + g.off(c * VEC), y, rd);
+        VecIO<T, VEC>::store(xl + g.off32(c * VEC), y, rd);
 #pragma unroll
         for (int e = 0; e < VEC; ++e) rs = fmaf(rd[e], rd[e], rs);
       }
     }
 #pragma unroll
     for (int e = 0; e < EPT; ++e) acc[e] = 0.f;
-    const float nn = sqrtf(consumer_sum(rs, red));
-    if (ct == 0) norm[mt.gid] = nn;
+    rs = warp_sum(rs);
+    if (lane == 0) red2[par * 8 + cw] = rs;
+    prev_norm = norm + mt.gid;
+    par ^= 1;
   }
 }
 
@@ -961,7 +1055,7 @@ template <typename T, int EPT>
 cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, const void* okn,
                       const void* ovn, int32_t* ws, int64_t n_total, int nbuf, int slot_bytes, ItemSel sel,
                       ExactArgs ex, cudaStream_t s) {
-  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + MG_MAX_BUF * (int)sizeof(SlotMeta) + 128;
+  const int smem = nbuf * slot_bytes + 2 * MG_MAX_BUF * 8 + MG_MAX_BUF * (int)sizeof(SlotMeta) + 256;
   static int attr = 0;  // per instantiation
   if (attr < smem) {
     cudaError_t e = cudaFuncSetAttribute(merge_tma_kernel<T, EPT>,
@@ -983,9 +1077,14 @@ cudaError_t merge_tma(void* pk, void* pv, const Geom& g, void* kn, void* vn, con
     const char* e = getenv("KVF_MERGE_CTAS_PER_SM");
     return e ? std::max(1, atoi(e)) : 2;
   }();
+  // exact mode: fp32 shadow rows stream through the ring as two half-row slots (a bf16
+  // slot holds r / 2 floats) instead of plain loads by the consumers; KVF_MERGE_SHADOW_DIRECT
+  // restores the plain loads (A/B)
+  static const bool direct = getenv("KVF_MERGE_SHADOW_DIRECT") != nullptr;
+  const int ring_shadow = ex.shadow && sizeof(T) == 2 && g.r() % 16 == 0 && !direct ? 1 : 0;
   merge_tma_kernel<T, EPT><<<per_sm * n_sm, MG_THREADS, smem, s>>>((T*)pk, (T*)pv, g, (float*)kn, (float*)vn,
                                                          (const float*)okn, (const float*)ovn, ws,
-                                                         n_total, nbuf, slot_bytes, sel, ex);
+                                                         n_total, nbuf, slot_bytes, sel, ex, ring_shadow);
   return cudaGetLastError();
 }
 
@@ -1004,8 +1103,10 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
   // 2 x 32 KB x 2 CTAs 17.5 ms per 2 steps); KVF_MERGE_NBUF overrides (measurements)
   const char* eb = getenv("KVF_MERGE_NBUF");
   const int64_t fit = std::min<int64_t>(MG_MAX_BUF, (200 * 1024 / per_sm) / slot_bytes);  // smem
-  const int nbuf = (int)std::min<int64_t>(
-      fit, eb ? std::max(2, atoi(eb)) : std::max<int64_t>(2, (128 * 1024 / per_sm) / slot_bytes));
+  // exact mode streams fp32 shadow rows as two slots each: one slot deeper (cfg2, 32 layers:
+  // merges 14.3 ms with 2 slots, 13.8 ms with 3)
+  const int64_t want = (128 * 1024 / per_sm) / slot_bytes + (ex.shadow && !g.head_mode ? 1 : 0);
+  const int nbuf = (int)std::min<int64_t>(fit, eb ? std::max(2, atoi(eb)) : std::max<int64_t>(2, want));
   const bool tma_ok = !std::is_same<T, double>::value && can_vectorize<T>(pk, g) &&
                       can_vectorize<T>(pv, g) && nbuf >= 2 && r <= 64 * MG_CONSUMERS &&
                       (g.d * (int64_t)sizeof(T)) % 16 == 0;

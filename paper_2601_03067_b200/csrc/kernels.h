@@ -89,10 +89,10 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s);
 //   list[n] absorber global ids          count (absorbers), cursor (members)
 // n = U * NB (all units). remap re-zeroes mcnt / mfill for the next level.
 struct LevelWs {
-  int32_t *mcnt, *mfill, *mstart, *members, *list, *count, *cursor;
+  int32_t *mcnt, *mfill, *mstart, *members, *list, *count, *cursor, *fetch;
   __host__ __device__ LevelWs(int32_t* ws, int64_t n)
       : mcnt(ws), mfill(ws + n), mstart(ws + 2 * n), members(ws + 3 * n), list(ws + 4 * n),
-        count(ws + 5 * n), cursor(ws + 5 * n + 1) {}
+        count(ws + 5 * n), cursor(ws + 5 * n + 1), fetch(ws + 5 * n + 2) {}
   static int64_t ints(int64_t n) { return 5 * n + 64; }
 };
 

@@ -1,0 +1,104 @@
+"""Warm per-launch breakdown of one cfg2-shaped fusion step: CUDA events around every
+C-ABI call of an eager FusionEngine.run (same stream, so the intervals tile the step).
+
+usage: python tools/step_breakdown.py [L] [B] [p] [exact:on|off]
+"""
+import collections
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2601_03067_b200 import _native as N  # noqa: E402
+from paper_2601_03067_b200.engine import FusionEngine, Geometry  # noqa: E402
+from paper_2601_03067_b200.schedule import bff_plan  # noqa: E402
+from paper_2601_03067_b200.workload import synthetic_kv  # noqa: E402
+
+L = int(sys.argv[1]) if len(sys.argv) > 1 else 32
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+p = int(sys.argv[3]) if len(sys.argv) > 3 else 256
+exact = (sys.argv[4] != "off") if len(sys.argv) > 4 else None
+t, h, d = 16, 8, 128
+Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=1000)
+Kt, Vt = Kt.reshape(-1), Vt.reshape(-1)
+geom = Geometry(L, B * p, t, h, d, 0)
+plan = bff_plan(B, p, None)
+eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, exact=exact)
+k, v = Kt.clone(), Vt.clone()
+
+_orig = N.call
+rec = []
+
+
+def timed(name, *a, **kw):
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _orig(name, *a, **kw)
+    e1.record()
+    rec.append((name, e0, e1))
+
+
+for it in range(3):
+    k.copy_(Kt)
+    v.copy_(Vt)
+    rec.clear()
+    N.call = timed if it == 2 else _orig
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    st = eng.run(k, v, 0.8)
+    s1.record()
+    torch.cuda.synchronize()
+N.call = _orig
+tot = collections.defaultdict(float)
+cnt = collections.Counter()
+seq = []
+for name, a, b in rec:
+    ms = a.elapsed_time(b)
+    tot[name] += ms
+    cnt[name] += 1
+    seq.append((name, ms))
+step = s0.elapsed_time(s1)
+print(f"L={L} B={B} p={p} exact={eng.exact} compact_from={eng.compact_from} step {step:.2f} ms "
+      f"(sum of calls {sum(tot.values()):.2f})")
+for name in sorted(tot, key=lambda n: -tot[n]):
+    print(f"  {tot[name]:8.2f} ms  {100 * tot[name] / step:5.1f}%  x{cnt[name]:<3d} {name}")
+print("sequence:")
+for name, ms in seq:
+    if ms > 0.05:
+        print(f"  {ms:8.3f}  {name}")
+
+# algorithmic merge bytes per level: items = (absorber, K|V); reads = absorber + members,
+# one write per item; exact mode: key vectors with a shadow row are read as fp32 rows and
+# every key absorber also writes its fp32 row
+U, NB = geom.units, geom.NB
+ab = st.absorber.long()
+vb = geom.r * 2
+seen_abs = torch.zeros((U, NB), dtype=torch.bool, device=ab.device)
+merge_ms = [ms for name, ms in seq if name == "kvf_merge_groups"]
+blk = torch.arange(NB, device=ab.device)
+for li, lv in enumerate(plan.levels):
+    m = torch.from_numpy(lv.row_merge).to(ab.device).long()[blk // plan.bpr]
+    mg = torch.from_numpy(lv.merges).to(ab.device).long()
+    ok = m >= 0
+    lb, mid = mg[m.clamp(min=0), 0], mg[m.clamp(min=0), 1]
+    member = ok & (blk >= mid) & (ab >= lb) & (ab < mid) & (ab != 0x7FFFFFFF)
+    member = member.expand(U, NB) if member.dim() == 1 else member
+    n_mem = int(member.sum())
+    absr = torch.zeros((U, NB), dtype=torch.bool, device=ab.device)
+    uu = torch.arange(U, device=ab.device)[:, None].expand(U, NB)
+    absr[uu[member], ab[member]] = True
+    n_abs = int(absr.sum())
+    base = 2 * (n_abs + n_mem) * vb + 2 * n_abs * vb  # K and V: reads + writes
+    extra = 0
+    if eng.exact:
+        sh_mem = int((member & seen_abs).sum())
+        sh_abs = int((absr & seen_abs).sum())
+        extra = (sh_mem + sh_abs) * vb + n_abs * 2 * vb  # fp32 reads (2x) + fp32 row writes
+    seen_abs |= absr
+    gb = (base + extra) / 1e9
+    ms = merge_ms[li] if li < len(merge_ms) else float("nan")
+    print(f"level {li + 1}: absorbers {n_abs} members {n_mem} merge bytes {gb:.2f} GB "
+          f"({ms:.3f} ms -> {gb / ms:.2f} TB/s algorithmic)")
