@@ -202,6 +202,18 @@ __device__ __forceinline__ TileInfo rec_info(const int32_t* r, int nt, int64_t u
   return t;
 }
 
+// 16-byte global -> shared copy on the LSU path (L2 only), completion tracked by an
+// mbarrier arrive-on (noinc: the barrier's expected count covers the arriving lanes)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ uint32_t cluster_addr(const void* p, uint32_t cta) {
   uint32_t r;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(cta));
@@ -246,7 +258,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               const int32_t* __restrict__ live, const int32_t* __restrict__ rank,
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
               float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3,
-              int nsplit, float* __restrict__ spart, int32_t* __restrict__ scnt) {
+              int nsplit, float* __restrict__ spart, int32_t* __restrict__ scnt,
+              const __nv_bfloat16* __restrict__ pool) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ int split_last_sh;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
@@ -259,6 +272,9 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   uint64_t* sched_empty = sched_full + SCHED_DEPTH;   // [SCHED_DEPTH], used on the leader
   int32_t* sched_rec = reinterpret_cast<int32_t*>(sched_empty + SCHED_DEPTH);  // [SCHED_DEPTH][kRec]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_rec + SCHED_DEPTH * kRec);
+  // gathered rows on the LSU path (gathered == 2): per-CTA completion of a stage's
+  // cp.async copies (both producer warps' lanes arrive on it)
+  uint64_t* full_loc = reinterpret_cast<uint64_t*>(meta + 448);  // [STAGES]
   // epilogue column metadata, double-buffered by tile parity: [2][BN] each
   float* inv_j_b = reinterpret_cast<float*>(meta + 512);
   int32_t* colmin_b = reinterpret_cast<int32_t*>(meta + 512 + 8 * BN);
@@ -292,10 +308,12 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
     }
+    for (int s = 0; s < STAGES; ++s) mbar_init(&full_loc[s], 64);
     for (int c = 0; c < 2 * BN; ++c) colmin_b[c] = kNone;
     for (int b = 0; b < SCHED_DEPTH; ++b) {
       mbar_init(&sched_full[b], 1);
-      mbar_init(&sched_empty[b], kSchedConsumers);
+      // + in LSU-gather mode: warp 2 of both CTAs (second producer) and the peer's relay
+      mbar_init(&sched_empty[b], kSchedConsumers + (gathered == 2 ? 3 : 0));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -310,7 +328,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || (gathered == 2 && warp == 2)) {
     // producer warp: lane 0 runs the tile scheduler; operand rows are loaded by
     // lane 0 (tiled boxes over the pool or the staged rows) or, in gathered
     // mode, by all 32 lanes with TMA gather4 (4 alive rows per lane per operand)
@@ -338,6 +356,39 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int layer = (int)(t.u / layer_div);
       const int head = g.head_mode ? (int)(t.u % g.h) : 0;
       const int mi0 = t.i0 + (int)crank * BM;
+      if (gathered == 2) {
+        // LSU gather: warp 0 copies this CTA's 128 A rows, warp 2 its 128 B rows; a warp
+        // instruction moves 4 rows x 128 B (lane = row (lane >> 3), 16-B chunk (lane & 7)),
+        // stored at the 128B-swizzled position TMA would use; positions past the merge's
+        // alive blocks repeat its last alive block (the epilogue masks them)
+        const int pw = warp == 0 ? 0 : 1;
+        const int sub = lane >> 3, ch = lane & 7;
+        const int64_t gb = t.u * g.NB;
+        const int nrow = pw == 0 ? t.pm - t.pl : t.pr - t.pm;
+        const int p0 = pw == 0 ? mi0 : t.j0 + (int)crank * BNH;
+        const int32_t* lv = live + gb + (pw == 0 ? t.pl : t.pm);
+        const char* base[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int id = lv[min(p0 + 4 * i + sub, nrow - 1)];
+          base[i] = reinterpret_cast<const char*>(pool) +
+                    ((int64_t)layer * g.NB + id) * g.E() * 2 + ch * 16;
+        }
+        const uint32_t o0 = (uint32_t)(sub * 128 + ((ch ^ sub) * 16));
+        const uint32_t o1 = (uint32_t)((sub + 4) * 128 + ((ch ^ (sub + 4)) * 16));
+        for (int ks = 0; ks < nk; ++ks, ++kk) {
+          const int s = kk % STAGES;
+          const uint32_t ph = (kk / STAGES) & 1;
+          if (lane == 0) mbar_wait(&empty_bar[s], ph ^ 1);
+          __syncwarp();
+          const uint32_t tile = smem_u32(smem + s * STAGE_BYTES + pw * A_BYTES);
+#pragma unroll
+          for (int i = 0; i < 32; ++i)  // rows 4i + sub: 8-row swizzle atoms at i/2 * 1024 B
+            cp_async16(tile + (uint32_t)(i >> 1) * 1024u + ((i & 1) ? o1 : o0), base[i] + ks * 128);
+          cp_async_arrive_noinc(&full_loc[s]);
+        }
+        continue;
+      }
       if (gathered) {
         // rows 4*lane .. 4*lane+3 of this CTA's A (left) and B (right) operand;
         // positions past the merge's alive blocks repeat its last alive block
@@ -389,6 +440,25 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
         tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA + (part == 2 ? lo_rows : 0));
         tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB + (part == 1 ? lo_rows : 0));
+      }
+    }
+  } else if (warp == 3 && !leader && gathered == 2) {
+    // LSU-gather relay (peer CTA): a stage's cp.async copies complete on this CTA's
+    // full_loc barrier; make them visible to the async proxy and tell the leader's MMA
+    if (lane == 0) {
+      uint32_t kk = 0;
+      for (uint32_t it = 0;; ++it) {
+        const int sl = it % SCHED_DEPTH;
+        mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
+        const int w = sched_rec[sl * kRec];
+        mbar_arrive_cluster(&sched_empty[sl], 0);
+        if (w < 0) break;
+        for (int ks = 0; ks < nk; ++ks, ++kk) {
+          const int s = kk % STAGES;
+          mbar_wait(&full_loc[s], (kk / STAGES) & 1);
+          fence_proxy_async_smem();
+          mbar_arrive_cluster(&full_bar[s], 0);
+        }
       }
     }
   } else if (warp == 3) {
@@ -453,6 +523,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
           const int s = kk % STAGES;
           const uint32_t ph = (kk / STAGES) & 1;
           mbar_wait(&full_bar[s], ph);
+          if (gathered == 2) {  // LSU gather: the peer's rows (relay above), then our own
+            mbar_wait(&full_loc[s], ph);
+            fence_proxy_async_smem();
+          }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
           const uint32_t sb = sa + A_BYTES;
@@ -793,7 +867,9 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   CUtensorMap tmap;
   const Geom& g = a.g;
   const bool compact = a.live != nullptr;
-  const bool gathered = compact && a.staged == nullptr;  // TMA gather4 over the pool
+  const bool gathered = compact && a.staged == nullptr;  // alive rows straight from the pool
+  // gathered rows: LSU cp.async (default) or TMA gather4 (KVF_GATHER4=1, A/B)
+  static const int gmode = getenv("KVF_GATHER4") ? 1 : 2;
   const bool staged = compact && !gathered;
   if (gathered && g.head_mode) return cudaErrorInvalidValue;
   const cuuint64_t r = (cuuint64_t)g.r();
@@ -864,8 +940,8 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
       tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
-      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? 1 : 0, split3 ? 1 : 0,
-      nsplit, a.split_part, a.split_count);
+      a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? gmode : 0, split3 ? 1 : 0,
+      nsplit, a.split_part, a.split_count, (const __nv_bfloat16*)a.pool);
   return cudaGetLastError();
 }
 

@@ -1,7 +1,7 @@
 """Warm per-launch breakdown of one cfg2-shaped fusion step: CUDA events around every
 C-ABI call of an eager FusionEngine.run (same stream, so the intervals tile the step).
 
-usage: python tools/step_breakdown.py [L] [B] [p] [exact:on|off]
+usage: python tools/step_breakdown.py [L] [B] [p] [exact:on|off] [compact_from|auto|none] [staged|gathered]
 """
 import collections
 import os
@@ -19,12 +19,16 @@ L = int(sys.argv[1]) if len(sys.argv) > 1 else 32
 B = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 p = int(sys.argv[3]) if len(sys.argv) > 3 else 256
 exact = (sys.argv[4] != "off") if len(sys.argv) > 4 else None
+cf = sys.argv[5] if len(sys.argv) > 5 else "auto"
+cf = None if cf == "none" else ("auto" if cf == "auto" else int(cf))
+cmode = sys.argv[6] if len(sys.argv) > 6 else "auto"
 t, h, d = 16, 8, 128
 Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=1000)
 Kt, Vt = Kt.reshape(-1), Vt.reshape(-1)
 geom = Geometry(L, B * p, t, h, d, 0)
 plan = bff_plan(B, p, None)
-eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, exact=exact)
+eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, exact=exact, compact_from=cf,
+                   compact_mode=cmode)
 k, v = Kt.clone(), Vt.clone()
 
 _orig = N.call
@@ -61,7 +65,8 @@ for name, a, b in rec:
     cnt[name] += 1
     seq.append((name, ms))
 step = s0.elapsed_time(s1)
-print(f"L={L} B={B} p={p} exact={eng.exact} compact_from={eng.compact_from} step {step:.2f} ms "
+print(f"L={L} B={B} p={p} exact={eng.exact} compact_from={eng.compact_from} mode={eng.compact_mode} "
+      f"CR {(U0 := geom.units * geom.NB) / max(int(st.live_count.sum()), 1):.6f} step {step:.2f} ms "
       f"(sum of calls {sum(tot.values()):.2f})")
 for name in sorted(tot, key=lambda n: -tot[n]):
     print(f"  {tot[name]:8.2f} ms  {100 * tot[name] / step:5.1f}%  x{cnt[name]:<3d} {name}")
