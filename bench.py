@@ -562,12 +562,13 @@ def ours_main(args):
     n_sim = sum(len(st.sim_events) for _, _, st in sim_recs) * len(recs) / len(sim_recs)
     st_last = recs[-1][2]
     # algorithmic similarity FLOPs: sum over merges of 2 * left_blocks * right_blocks * r
-    flops = 0.0
+    flops = executed = 0.0
     for _, _, st in sim_recs:
-        for s in st.level_stats:
-            s = s.double()
-            flops += float((2.0 * s[..., 0] * s[..., 1]).sum().item()) * geom.r
+        w = sim_work(st, engine)
+        flops += w["flops"]
+        executed += w["executed"]
     flops *= len(recs) / len(sim_recs)
+    executed *= len(recs) / len(sim_recs)
     tmax = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         reduce_max(dist, tmax)
@@ -644,6 +645,11 @@ def ours_main(args):
                 "traffic": traffic,
                 "peak_source": peak_source,
                 "work": "algorithmic FLOPs = sum_merges 2*left_blocks*right_blocks*r (MergeRecord counts)",
+                "executed_tflops": executed / (sim_ms / 1e3) / 1e12 if sim_ms > 0 else 0.0,
+                "executed_frac": (executed / (sim_ms / 1e3) / 1e12 / tc_peak) if sim_ms > 0 and tc_peak else None,
+                "useful_fraction": flops / executed if executed else None,
+                "executed_note": "tensor-core FLOPs of the 256 x 256 tiles actually run (dead rows inside the "
+                                 "uncompacted levels' rectangles and tile padding included)",
                 "sim_ms_per_step": sim_ms / args.steps,
                 "sim_launches_per_step": n_sim / args.steps,
                 "sim_timing": ("CUDA events around each similarity launch of the timed steps"
@@ -698,9 +704,12 @@ def ours_main(args):
     # ---- the other single-GPU BASELINE configurations, each with its own parity leg ----
     if rank == 0 and world == 1 and args.config == "cfg2" and not args.skip_configs:
         out["configs"] = {}
-        for name in ("cfg1", "cfg3"):
+        for name in ("cfg1", "cfg3", "cfg5"):
             try:
-                out["configs"][name] = bench_subconfig(name, dev, torch, skip_cpu=args.skip_cpu)
+                if name == "cfg5":
+                    out["configs"][name] = bench_cfg5_layer(dev, torch)
+                else:
+                    out["configs"][name] = bench_subconfig(name, dev, torch, skip_cpu=args.skip_cpu)
             except Exception as exc:  # reported, never fatal
                 out["configs"][name] = {"error": str(exc)[-400:]}
             torch.cuda.empty_cache()
@@ -709,6 +718,40 @@ def ours_main(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def sim_work(st, engine) -> dict:
+    """Similarity work of one fusion run from its MergeRecord counters (level_stats[..., 0:2] =
+    alive fusable left / right blocks per merge):
+      flops     algorithmic: sum_merges 2 * left * right * r (what `roofline.achieved` uses)
+      executed  tensor-core FLOPs of the 256 x 256 tiles the kernel runs: full merge rectangles
+                over pool rows, or over the alive rows at compacted levels (x3 for float32 hi/lo)
+      bytes     operand bytes if every alive row were read once per level (the HBM floor)"""
+    import math
+
+    g = engine.geom
+    flops = executed = nbytes = 0.0
+    tm, tn = engine.tm, engine.tn
+    split = 3 if engine.filter_mode else 1
+    esize = 4 if engine.filter_mode else 2  # bf16 operand (float32 pools: hi + lo copies)
+    for li, s in enumerate(st.level_stats):
+        s = s.double()
+        nl, nr = s[..., 0], s[..., 1]
+        flops += float((2.0 * nl * nr).sum().item()) * g.r
+        nbytes += float((nl + nr).sum().item()) * g.r * esize
+        lv = engine.plan.levels[li]
+        if engine.compact_from is not None and lv.height >= engine.compact_from:
+            tiles = float((torch_ceil_div(nl, tm) * torch_ceil_div(nr, tn)).sum().item())
+        else:
+            m = lv.merges
+            tiles = float(sum(math.ceil((b - a) / tm) * math.ceil((c - b) / tn) for a, b, c in m.tolist()))
+            tiles *= g.units
+        executed += tiles * 2.0 * tm * tn * g.r * split
+    return {"flops": flops, "executed": executed, "bytes": nbytes}
+
+
+def torch_ceil_div(x, n):
+    return (x + (n - 1)).div(n, rounding_mode="floor")
 
 
 def gpu_parity_state(st, plan, layers):
@@ -815,20 +858,28 @@ def bench_subconfig(name, dev, torch, steps=10, warmup=3, skip_cpu=False):
             times.append((e0, e1))
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in times) / steps
-    sim_ms, flops = 0.0, 0.0
+    sim_ms, flops, executed, obytes = 0.0, 0.0, 0.0, 0.0
     for _ in range(steps):
         Kw.copy_(K0)
         Vw.copy_(V0)
         st_e = eng.run(Kw.view(-1), Vw.view(-1), c["thr"], time_sim=True)
         torch.cuda.synchronize()
         sim_ms += sum(a.elapsed_time(b) for a, b, _ in st_e.sim_events)
-        flops += sum(float((2.0 * s[..., 0].double() * s[..., 1].double()).sum()) for s in st_e.level_stats) * geom.r
+        w = sim_work(st_e, eng)
+        flops += w["flops"]
+        executed += w["executed"]
+        obytes += w["bytes"]
     sim_ms /= steps
     flops /= steps
+    executed /= steps
+    obytes /= steps
     live = int(st.live_count.sum())
     pk = peaks()
     tc_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    hbm_peak = pk.get("hbm_gbs")
     achieved = flops / (sim_ms / 1e3) / 1e12 if sim_ms else 0.0
+    exe_tf = executed / (sim_ms / 1e3) / 1e12 if sim_ms else 0.0
+    gbs = obytes / (sim_ms / 1e3) / 1e9 if sim_ms else 0.0
     kvb = kv_bytes(c, elem)
     res = {
         "workload": c["workload"], "metric": METRIC, "value": kvb / (ms / 1e3) / 1e9, "unit": "GB/s",
@@ -841,23 +892,32 @@ def bench_subconfig(name, dev, torch, steps=10, warmup=3, skip_cpu=False):
         "compression_ratio": L * B * p / live,
         "sim_path": st.path_name,
         "split_k": eng.nsplit,
+        # both configurations sit below the bf16 ridge (cfg1 ~38, cfg3 ~150 FLOP/B):
+        # the similarity launches are bounded by reading every alive K row once per level
         "roofline": {
             "kernel": "sim_tc_kernel (similarity + first-match epilogue, incl. the float64 re-score launch)",
-            "bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
-            "frac": achieved / tc_peak if tc_peak else None, "sim_ms_per_step": sim_ms,
-            "share_of_step": sim_ms / ms if ms else None,
-            "work": "sum_merges 2*left_blocks*right_blocks*r" + (" (float32: executed as 3 bf16 hi/lo "
-                                                                  "passes, 3x these FLOPs)"
-                                                                  if dtype == torch.float32 else ""),
+            "bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+            "frac": gbs / hbm_peak if hbm_peak else None, "traffic": None,
+            "work": ("operand bytes = sum over levels of (alive left + alive right blocks) x r x "
+                     + ("4 B (bf16 hi + lo copies of the float32 pool)" if dtype == torch.float32 else "2 B")
+                     + ": every alive K row read once per level"),
+            "sim_ms_per_step": sim_ms, "share_of_step": sim_ms / ms if ms else None,
+            "tensor": {"achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                       "frac": achieved / tc_peak if tc_peak else None, "executed_tflops": exe_tf,
+                       "work": "sum_merges 2*left_blocks*right_blocks*r" + (
+                           " (float32: executed as 3 bf16 hi/lo passes)" if dtype == torch.float32 else "")},
         },
     }
     if c["dtype"] == "fp32":
         mhz = 1965
-        res["roofline"]["fp32_cuda_core_peak"] = 148 * 128 * 2 * mhz * 1e6 / 1e12
-        res["roofline"]["frac_of_fp32_cuda_core_peak"] = achieved / res["roofline"]["fp32_cuda_core_peak"]
-    if c["variant"] == "cff":  # CFF levels re-read K: the HBM roofline bounds them
-        res["roofline"]["note"] = ("CFF merges are 128 x 128 blocks at level 1 (25% of a 256 x 256 tile) and "
-                                   "the step is HBM-bound: 2.1 GB of K+V per step")
+        res["roofline"]["tensor"]["fp32_cuda_core_peak"] = 148 * 128 * 2 * mhz * 1e6 / 1e12
+        res["roofline"]["tensor"]["frac_of_fp32_cuda_core_peak"] = (
+            achieved / res["roofline"]["tensor"]["fp32_cuda_core_peak"])
+        res["roofline"]["note"] = ("4 layers x 512 blocks: 3 levels of 16 / 8 / 4 tiles (split-K over all SMs); "
+                                   "each launch is a few microseconds of work, so launch latency bounds it")
+    if c["variant"] == "cff":
+        res["roofline"]["note"] = ("CFF level-1 merges are 128 x 128 blocks inside 256 x 256 tiles; the step "
+                                   "moves 2.1 GB of K+V for norms and ~3 GB of operand rows for similarity")
     layers = list(range(min(L, ref_concurrency(name, cap=8))))
     par = gpu_parity_state(st, plan, layers)
     res["parity"] = {"exact_mode": bool(st.exact), "inexact_pairs_per_step": st.inexact_pairs()}
@@ -874,6 +934,76 @@ def bench_subconfig(name, dev, torch, steps=10, warmup=3, skip_cpu=False):
             res["parity"] = parity_vs_reference(par, ref, layers, res["parity"])
         except Exception as exc:  # reported, never fatal
             res["cpu_baseline"] = {"value": None, "error": str(exc)[-300:]}
+    return res
+
+
+def bench_cfg5_layer(dev, torch, steps=2, warmup=1):
+    """BASELINE configs[4] on one GPU: one Llama-3-70B-shaped layer (batch 256 x 16K: 262,144
+    blocks of 32 KB per K and V, 17.2 GB) fused at full shape. Layers fuse independently
+    (fusion.py:367-374), so the 80-layer step is 80 x this layer on one GPU and 80 / N layers
+    per rank when layer-sharded (`bench.py --config cfg5` under torchrun runs that)."""
+    from paper_2601_03067_b200.engine import FusionEngine, Geometry
+    from paper_2601_03067_b200.schedule import bff_plan
+    from paper_2601_03067_b200.workload import synthetic_kv
+
+    c = CONFIGS["cfg5"]
+    L, B, p, t, h, d = c["L"], c["B"], c["p"], c["t"], c["h"], c["d"]
+    geom = Geometry(1, B * p, t, h, d, 0)
+    K0, V0 = synthetic_kv(1, B, p, t, h, d, dtype=torch.bfloat16, seed=3000, device=dev)
+    Kw, Vw = torch.empty_like(K0), torch.empty_like(V0)
+    eng = FusionEngine(geom, bff_plan(B, p, None), torch.bfloat16, dev)
+    times, sim_ms, flops, executed = [], 0.0, 0.0, 0.0
+    for i in range(warmup + steps):
+        Kw.copy_(K0)
+        Vw.copy_(V0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = eng.run(Kw.view(-1), Vw.view(-1), c["thr"], time_sim=i >= warmup)
+        e1.record()
+        torch.cuda.synchronize()
+        if i >= warmup:
+            times.append(e0.elapsed_time(e1))
+            sim_ms += sum(a.elapsed_time(b) for a, b, _ in st.sim_events)
+            w = sim_work(st, eng)
+            flops += w["flops"]
+            executed += w["executed"]
+    ms = sum(times) / steps
+    sim_ms /= steps
+    flops /= steps
+    executed /= steps
+    live = int(st.live_count.sum())
+    pk = peaks()
+    tc_peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    layer_bytes = 2 * B * p * t * h * d * 2
+    res = {
+        "workload": c["workload"], "metric": METRIC, "unit": "GB/s",
+        "value": layer_bytes / (ms / 1e3) / 1e9,
+        "ms_per_layer": ms, "ms_per_step_1gpu": ms * L, "steps": steps, "warmup": warmup, "dtype": "bf16",
+        "config": {"L": L, "B": B, "p": p, "t": t, "h": h, "d": d, "variant": "bff", "threshold": c["thr"],
+                   "layers_timed": 1,
+                   "timing": "CUDA events around FusionEngine.run of one full-shape layer (262,144 blocks); "
+                             "pristine layer restored (untimed) before each step",
+                   "step": "80 layers = 80 x the layer time on one GPU (layers are independent, "
+                           "fusion.py:367-374); layer-sharded over N GPUs: ceil(80 / N) layers per rank",
+                   "l2": "per-layer K+V 17.2 GB >> 126 MB L2"},
+        "compression_ratio": B * p / max(live, 1),
+        "sim_path": st.path_name,
+        "compact_from_height": eng.compact_from,
+        "roofline": {"kernel": "sim_tc_kernel (K2+K3 similarity GEMM + first-match epilogue)", "bound": "tensor",
+                     "achieved": flops / (sim_ms / 1e3) / 1e12 if sim_ms else 0.0, "peak": tc_peak,
+                     "unit": "TFLOP/s",
+                     "frac": flops / (sim_ms / 1e3) / 1e12 / tc_peak if sim_ms and tc_peak else None,
+                     "executed_tflops": executed / (sim_ms / 1e3) / 1e12 if sim_ms else 0.0,
+                     "sim_ms_per_layer": sim_ms, "share_of_step": sim_ms / ms if ms else None,
+                     "work": "sum_merges 2*left_blocks*right_blocks*r"},
+        "parity": {"exact_mode": bool(st.exact), "inexact_pairs": st.inexact_pairs(),
+                   "inexact_blocks": st.inexact_blocks(),
+                   "vs_reference": "not run: one float64 reference layer of this shape needs ~70 GB of host "
+                                   "RAM and days of CPU time; decisions follow the same exact-mode rule that "
+                                   "matches the reference bit for bit at cfg1 / cfg2 / cfg3"},
+    }
+    del K0, V0, Kw, Vw, eng, st
+    torch.cuda.empty_cache()
     return res
 
 
@@ -1272,7 +1402,7 @@ def main():
                          "cpu_baseline leg (bounded by host RAM and cores)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-decode", action="store_true")
-    ap.add_argument("--skip-configs", action="store_true", help="skip the cfg1 / cfg3 sub-blocks")
+    ap.add_argument("--skip-configs", action="store_true", help="skip the cfg1 / cfg3 / cfg5 sub-blocks")
     ap.add_argument("--cpu-sample", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--cpu-decode-sample", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--layers", default="0", help=argparse.SUPPRESS)
