@@ -19,6 +19,17 @@ for hm in ("folded", "per_head"):
     outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8, head_mode=hm), keep_samples=True)
     torch.cuda.synchronize()
     print("bf16", hm, sum(o.report.blocks_before for o in outs) / sum(o.report.blocks_after for o in outs))
+# compacted levels with the alive rows gathered from the pool (cp.async + peer relay)
+from paper_2601_03067_b200 import _native as N  # noqa: E402
+from paper_2601_03067_b200.engine import FusionEngine, Geometry  # noqa: E402
+from paper_2601_03067_b200.schedule import bff_plan  # noqa: E402
+
+Kt, Vt = synthetic_kv(1, 16, 64, 16, 8, 128, dtype=torch.bfloat16, seed=9)
+eng = FusionEngine(Geometry(1, 16 * 64, 16, 8, 128, 0), bff_plan(16, 64, None), torch.bfloat16, Kt.device,
+                   N.PATH_TC, compact_from=2, compact_mode="gathered")
+st = eng.run(Kt.reshape(-1).clone(), Vt.reshape(-1).clone(), 0.8)
+torch.cuda.synchronize()
+print("gathered", int(st.live_count.sum()))
 # float32: split operands, split-K (few long tiles)
 Kt, Vt = synthetic_kv(2, 8, 64, 16, 8, 128, dtype=torch.float32, seed=6)
 cache = K.PagedKvCache(K.CacheDims(B=8, p=64, t=16, h=8, d=128, L=2), Kt, Vt)
