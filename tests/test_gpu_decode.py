@@ -102,6 +102,8 @@ def test_scheduled_decode_vs_reference(d, G, head_mode, ib):
             for hu in range(nh):
                 u = layer * h + hu if head_mode == "per_head" else layer
                 tab, ksc, vsc = st.table[u].cpu(), st.k_scale[u].cpu(), st.v_scale[u].cpu()
+                valid_slots = torch.cat([b * p + torch.arange(int(nblk[b])) for b in range(B)])
+                refs = torch.bincount(tab[valid_slots].long(), minlength=tab.numel())
                 meta = sched.meta[hu, :n_valid].cpu().long()
                 phys = sched.phys[hu, :n_valid].cpu()
                 # items swept by the physical block of their middle slot
@@ -118,7 +120,11 @@ def test_scheduled_decode_vs_reference(d, G, head_mode, ib):
                     assert (phys[row, n:] == -1).all()
                     slots = b * p + pos
                     assert torch.equal(phys[row, :n], tab[slots])
-                    assert torch.equal(sched.ks[hu, row, :n].cpu(), ksc[slots])
+                    # K scale magnitudes; the sign bit flags blocks that no other valid slot
+                    # of the unit references (the decode's L2 evict-first hint)
+                    ks_row = sched.ks[hu, row, :n].cpu()
+                    assert torch.equal(ks_row.abs(), ksc[slots])
+                    assert torch.equal(torch.signbit(ks_row), refs[tab[slots].long()] == 1)
                     assert torch.equal(sched.vs[hu, row, :n].cpu(), vsc[slots])
                 for b in range(B):
                     n = int(nblk[b])
