@@ -23,10 +23,18 @@ cf = sys.argv[5] if len(sys.argv) > 5 else "auto"
 cf = None if cf == "none" else ("auto" if cf == "auto" else int(cf))
 cmode = sys.argv[6] if len(sys.argv) > 6 else "auto"
 t, h, d = 16, 8, 128
-Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=1000)
+variant = os.environ.get("VARIANT", "bff")  # cff: chunks of 2048 tokens (cfg3 = 32 1 1024)
+Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=1000, variant=variant)
 Kt, Vt = Kt.reshape(-1), Vt.reshape(-1)
-geom = Geometry(L, B * p, t, h, d, 0)
-plan = bff_plan(B, p, None)
+geom = Geometry(L, B * p, t, h, d, int(os.environ.get("HEAD_MODE", "0")))
+if variant == "cff":
+    from paper_2601_03067_b200.core import cff_layout
+    from paper_2601_03067_b200.schedule import cff_plan
+
+    C, bpc = cff_layout(p, t, 2048)
+    plan = cff_plan(B, C, bpc, None)
+else:
+    plan = bff_plan(B, p, None)
 eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, exact=exact, compact_from=cf,
                    compact_mode=cmode)
 k, v = Kt.clone(), Vt.clone()
@@ -107,3 +115,40 @@ for li, lv in enumerate(plan.levels):
     ms = merge_ms[li] if li < len(merge_ms) else float("nan")
     print(f"level {li + 1}: absorbers {n_abs} members {n_mem} merge bytes {gb:.2f} GB "
           f"({ms:.3f} ms -> {gb / ms:.2f} TB/s algorithmic)")
+
+# similarity work per level: algorithmic FLOPs (alive fusable pairs) vs executed FLOPs
+# (active 256 x 256 tiles: full rectangles over pool rows, or over alive rows when compacted)
+sim_ms = collections.defaultdict(float)
+lvl_of = []
+li = 0
+for name, ms in seq:
+    if name == "kvf_similarity_select":
+        sim_ms[li] += ms
+    if name == "kvf_merge_groups":
+        li += 1
+alive_hist = []  # alive flags before each level, reconstructed from the absorber record
+alive = torch.ones((U, NB), dtype=torch.bool, device=ab.device)
+for li, lv in enumerate(plan.levels):
+    s_ = st.level_stats[li].double()
+    alg = float((2 * s_[..., 0] * s_[..., 1]).sum()) * geom.r
+    mg = torch.from_numpy(lv.merges).to(ab.device).long()
+    compact = eng.compact_from is not None and lv.height >= eng.compact_from
+    ex_tiles = 0
+    cum = torch.cat([torch.zeros((U, 1), dtype=torch.long, device=ab.device), alive.long().cumsum(1)], 1)
+    for lb_, mid_, re_ in mg.tolist():
+        if compact:
+            nl = (cum[:, mid_] - cum[:, lb_]).clamp(min=0)
+            nr = (cum[:, re_] - cum[:, mid_]).clamp(min=0)
+        else:
+            nl = torch.full((U,), mid_ - lb_, device=ab.device)
+            nr = torch.full((U,), re_ - mid_, device=ab.device)
+        ex_tiles += int(((nl + 255) // 256 * ((nr + 255) // 256)).sum())
+    exe = ex_tiles * 2.0 * 256 * 256 * geom.r
+    ms = sim_ms[li]
+    print(f"level {li + 1}: sim {ms:.3f} ms  algorithmic {alg / 1e12:.2f} TFLOP ({alg / ms / 1e9:.0f} TF/s)  "
+          f"executed {exe / 1e12:.2f} TFLOP ({exe / ms / 1e9:.0f} TF/s, {alg / exe:.2f} useful)")
+    # blocks absorbed at this level die before the next
+    m = torch.from_numpy(lv.row_merge).to(ab.device).long()[blk // plan.bpr]
+    lb, mid = mg[m.clamp(min=0), 0], mg[m.clamp(min=0), 1]
+    member = (m >= 0) & (blk >= mid) & (ab >= lb) & (ab < mid) & (ab != 0x7FFFFFFF)
+    alive &= ~member
