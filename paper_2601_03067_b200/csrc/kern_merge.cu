@@ -769,15 +769,17 @@ merge_warp_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g,
 // ---------------------------------------------------------------------------
 struct RingSlotMeta {
   float inv, home;
-  int32_t gid, flags;  // flags: bit0 last vector of the item, bit1 V tensor
+  int32_t gid, flags;  // flags: bit0 last slot of the item, bit1 V tensor
   int32_t sh, ash;     // exact mode, keys: the vector's / the absorber's shadow row (-1: none)
+  int32_t half;        // exact mode: 1 / 2 = first / second half of the fp32 shadow row sh
+                       // in the slot (ring-fed), -1 = read row sh from global, 0 = pool vector
 };
 template <int CPL, int NS>
 __global__ void __launch_bounds__(256, 2)
 merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict__ pool_v, Geom g,
                   float* __restrict__ knorm, float* __restrict__ vnorm,
                   const float* __restrict__ oknorm, const float* __restrict__ ovnorm,
-                  int32_t* ws, int64_t n_total, ItemSel sel, ExactArgs ex) {
+                  int32_t* ws, int64_t n_total, ItemSel sel, ExactArgs ex, int ring_shadow) {
   constexpr int VB = CPL * 512;  // vector bytes (32 lanes x CPL x 16 B)
   extern __shared__ __align__(128) uint8_t rsm[];
   const LevelWs W(ws, n_total);
@@ -843,28 +845,55 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
       sh = (ex.shadow && !is_v) ? ex.sidx[gb + id] : -1;
       if (sh >= 0) inv = 1.f;
     }
+    // the warp consumes slot q_c while issuing: a vector may only take slots the consumer
+    // has released (q_i + need - q_c <= NS); a shadow row needing two waits a round
+    if (q_i + ((sh >= 0 && ring_shadow) ? 2u : 1u) - q_c > (uint32_t)NS) return;
     const int s = q_i % NS;
     const int64_t u = gid_i / g.NB;
-    if (lane == 0) {
-      RingSlotMeta m;
-      m.inv = inv;
-      m.home = home_i;
-      m.gid = (int32_t)gid_i;
-      m.flags = (v_i == n_i ? 1 : 0) | (is_v ? 2 : 0);
-      m.sh = sh;
-      m.ash = ash_i;
-      smeta[s] = m;
-      if (sh >= 0)
-        mbar_arrive(&bars[s]);  // shadow row: the consumer reads it from global memory
-      else
-        mbar_expect_tx(&bars[s], (uint32_t)VB);  // release: slot meta visible after the wait
+    if (sh >= 0 && ring_shadow) {
+      // fp32 shadow row (2 * VB bytes): two slots of VB bytes, one bulk copy each
+      if (lane == 0) {
+        const char* row = reinterpret_cast<const char*>(ex.shadow + (int64_t)sh * g.r());
+        for (int hf = 0; hf < 2; ++hf) {
+          const int sl = (q_i + hf) % NS;
+          RingSlotMeta m;
+          m.inv = inv;
+          m.home = home_i;
+          m.gid = (int32_t)gid_i;
+          m.flags = (hf == 1 && v_i == n_i ? 1 : 0) | (is_v ? 2 : 0);
+          m.sh = sh;
+          m.ash = ash_i;
+          m.half = 1 + hf;
+          smeta[sl] = m;
+          mbar_expect_tx(&bars[sl], (uint32_t)VB);
+          bulk_g2s(ring + (size_t)sl * VB, row + (size_t)hf * VB, (uint32_t)VB, &bars[sl]);
+        }
+      }
+      __syncwarp();
+      q_i += 2;
+    } else {
+      if (lane == 0) {
+        RingSlotMeta m;
+        m.inv = inv;
+        m.home = home_i;
+        m.gid = (int32_t)gid_i;
+        m.flags = (v_i == n_i ? 1 : 0) | (is_v ? 2 : 0);
+        m.sh = sh;
+        m.ash = ash_i;
+        m.half = sh >= 0 ? -1 : 0;
+        smeta[s] = m;
+        if (sh >= 0)
+          mbar_arrive(&bars[s]);  // shadow row: the consumer reads it from global memory
+        else
+          mbar_expect_tx(&bars[s], (uint32_t)VB);  // release: slot meta visible after the wait
+      }
+      __syncwarp();
+      if (sh < 0 && lane < g.t) {
+        const __nv_bfloat16* src = (is_v ? pool_v : pool_k) + g.base(u, id) + lane * rstride;
+        bulk_g2s(ring + (size_t)s * VB + lane * segb, src, segb, &bars[s]);
+      }
+      ++q_i;
     }
-    __syncwarp();
-    if (sh < 0 && lane < g.t) {
-      const __nv_bfloat16* src = (is_v ? pool_v : pool_k) + g.base(u, id) + lane * rstride;
-      bulk_g2s(ring + (size_t)s * VB + lane * segb, src, segb, &bars[s]);
-    }
-    ++q_i;
     if (++v_i > n_i) {
       v_i = 0;
       it_i += nw;
@@ -885,7 +914,18 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
     mbar_wait(&bars[s], (q_c / NS) & 1);
     const RingSlotMeta m = smeta[s];
     const uint4* sp = reinterpret_cast<const uint4*>(ring + (size_t)s * VB);
-    if (m.sh >= 0) {  // exact mode: fused key member, its fp32 unit direction
+    if (m.half > 0) {  // exact mode: half of a fused key member's fp32 unit direction
+      const float* hs = reinterpret_cast<const float*>(ring + (size_t)s * VB);
+      const int q0 = m.half == 1 ? 0 : CPL / 2;
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        if (q < q0 || q >= q0 + CPL / 2) continue;  // static per unrolled q
+        const float4 a = *reinterpret_cast<const float4*>(hs + ((q - q0) * 32 + lane) * 8);
+        const float4 b = *reinterpret_cast<const float4*>(hs + ((q - q0) * 32 + lane) * 8 + 4);
+        acc[q][0] += a.x; acc[q][1] += a.y; acc[q][2] += a.z; acc[q][3] += a.w;
+        acc[q][4] += b.x; acc[q][5] += b.y; acc[q][6] += b.z; acc[q][7] += b.w;
+      }
+    } else if (m.sh >= 0) {  // exact mode: fused key member, its fp32 unit direction
       const float* row = ex.shadow + (int64_t)m.sh * g.r();
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {
@@ -1143,9 +1183,13 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
         const int smem = wpb * ns * (int)vbytes + wpb * ns * (8 + (int)sizeof(RingSlotMeta));
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
+        // exact mode: fp32 shadow rows through the ring as two half-row slots
+        // (KVF_MERGE_SHADOW_DIRECT: plain loads by the consuming warp, A/B)
+        static const bool direct = getenv("KVF_MERGE_SHADOW_DIRECT") != nullptr;
+        const int ring_shadow = ex.shadow && !direct ? 1 : 0;  // CPL = 4 or 8: even halves
         kern<<<148 * per_sm, wpb * 32, smem, s>>>((__nv_bfloat16*)pk, (__nv_bfloat16*)pv, g, (float*)kn,
                                                   (float*)vn, (const float*)okn, (const float*)ovn, ws,
-                                                  n_total, sel, ex);
+                                                  n_total, sel, ex, ring_shadow);
         return cudaGetLastError();
       };
       // measured (cfg2 per-head, 2 steps): 8 warps x 3 slots x 2 CTAs/SM 23.6 ms; 6 x 4 x 2 28.6;
