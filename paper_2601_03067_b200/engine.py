@@ -16,6 +16,8 @@ _fuse_layer (fusion.py:290-336), restated level-synchronously.
 
 from __future__ import annotations
 
+import os
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -459,6 +461,11 @@ STAGE_BUDGET = 4 << 30  # bytes of staged alive K rows (compacted levels, unit c
 _TILE_PART_BYTES = 256 * 256 * 4  # one CTA pair's fp32 accumulator tile
 
 
+# at most 8 k-splits: the last-arriving CTA sums the splits serially (cfg1 per-level similarity
+# with max 16 / 8 / 4 / 2 / 1 splits: 0.376 / 0.350 / 0.381 / 0.55 / 0.90 ms per step); KVF_SPLIT_MAX A/B
+SPLIT_MAX = int(os.environ.get("KVF_SPLIT_MAX", "8"))
+
+
 def choose_split(n_tiles: int, nk_run: int, pairs: int) -> int:
     """k-splits per tile for a similarity launch: levels with at most half a wave of
     tiles and long K (folded units: r / 64 k-steps, x3 for float32 hi/lo operands) are
@@ -469,7 +476,7 @@ def choose_split(n_tiles: int, nk_run: int, pairs: int) -> int:
     if n_tiles <= 0 or 2 * n_tiles > pairs or nk_run < 64:
         return 1
     best, best_cost = 1, float(-(-n_tiles // pairs))
-    for s in range(2, min(16, nk_run // 32) + 1):
+    for s in range(2, min(SPLIT_MAX, nk_run // 32) + 1):
         cost = -(-(n_tiles * s) // pairs) / s * (1.0 + 0.02 * s)
         if cost < best_cost - 1e-9:
             best, best_cost = s, cost

@@ -24,7 +24,8 @@ cf = None if cf == "none" else ("auto" if cf == "auto" else int(cf))
 cmode = sys.argv[6] if len(sys.argv) > 6 else "auto"
 t, h, d = 16, 8, 128
 variant = os.environ.get("VARIANT", "bff")  # cff: chunks of 2048 tokens (cfg3 = 32 1 1024)
-Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=1000, variant=variant)
+DT = torch.float32 if os.environ.get("DTYPE") == "f32" else torch.bfloat16  # cfg1: DTYPE=f32 4 8 64
+Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=DT, seed=1000, variant=variant)
 Kt, Vt = Kt.reshape(-1), Vt.reshape(-1)
 geom = Geometry(L, B * p, t, h, d, int(os.environ.get("HEAD_MODE", "0")))
 if variant == "cff":
@@ -35,7 +36,7 @@ if variant == "cff":
     plan = cff_plan(B, C, bpc, None)
 else:
     plan = bff_plan(B, p, None)
-eng = FusionEngine(geom, plan, torch.bfloat16, Kt.device, N.PATH_TC, exact=exact, compact_from=cf,
+eng = FusionEngine(geom, plan, DT, Kt.device, N.PATH_TC, exact=exact, compact_from=cf,
                    compact_mode=cmode)
 k, v = Kt.clone(), Vt.clone()
 
@@ -88,7 +89,7 @@ for name, ms in seq:
 # every key absorber also writes its fp32 row
 U, NB = geom.units, geom.NB
 ab = st.absorber.long()
-vb = geom.r * 2
+vb = geom.r * Kt.element_size()
 seen_abs = torch.zeros((U, NB), dtype=torch.bool, device=ab.device)
 merge_ms = [ms for name, ms in seq if name == "kvf_merge_groups"]
 blk = torch.arange(NB, device=ab.device)
