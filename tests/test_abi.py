@@ -74,8 +74,9 @@ def test_schedule_and_compaction_argument_errors():
     """New entry points validate before touching the GPU."""
     lib = N.lib()
     assert lib.kvf_decode_schedule_item_blocks() in (8, 16)
-    assert lib.kvf_decode_schedule_ws_ints(0, 8, 1024, 4, 256, 16) == 1024 + 4 * 16
-    assert lib.kvf_decode_schedule_ws_ints(1, 8, 1024, 4, 256, 8) == 8 * 1024 + 8 * 4 * 32
+    # per head unit: block histogram + block reference counts (L2 policy) + item keys
+    assert lib.kvf_decode_schedule_ws_ints(0, 8, 1024, 4, 256, 16) == 2 * 1024 + 4 * 16
+    assert lib.kvf_decode_schedule_ws_ints(1, 8, 1024, 4, 256, 8) == 8 * 2 * 1024 + 8 * 4 * 32
     assert lib.kvf_decode_schedule_ws_ints(0, 8, 1024, 4, 256, 5) < 0  # bad item size
     # B * p_blocks beyond the layer's slots
     rc = lib.kvf_decode_schedule(None, None, None, 1, 100, 16, 8, 128, 0, 0, 4, 32, None, 16,
