@@ -648,7 +648,7 @@ def ours_main(args):
                 "executed_tflops": executed / (sim_ms / 1e3) / 1e12 if sim_ms > 0 else 0.0,
                 "executed_frac": (executed / (sim_ms / 1e3) / 1e12 / tc_peak) if sim_ms > 0 and tc_peak else None,
                 "useful_fraction": flops / executed if executed else None,
-                "executed_note": "tensor-core FLOPs of the 256 x 256 tiles actually run (dead rows inside the "
+                "executed_note": "tensor-core FLOPs of the tiles actually run (256 x 256; 512 x 256 on the wide levels) (dead rows inside the "
                                  "uncompacted levels' rectangles and tile padding included)",
                 "sim_ms_per_step": sim_ms / args.steps,
                 "sim_launches_per_step": n_sim / args.steps,
@@ -724,14 +724,15 @@ def sim_work(st, engine) -> dict:
     """Similarity work of one fusion run from its MergeRecord counters (level_stats[..., 0:2] =
     alive fusable left / right blocks per merge):
       flops     algorithmic: sum_merges 2 * left * right * r (what `roofline.achieved` uses)
-      executed  tensor-core FLOPs of the 256 x 256 tiles the kernel runs: full merge rectangles
+      executed  tensor-core FLOPs of the tiles the kernel runs (256 x 256, or 512 x 256 at the
+                levels on the wide tile): full merge rectangles
                 over pool rows, or over the alive rows at compacted levels (x3 for float32 hi/lo)
       bytes     operand bytes if every alive row were read once per level (the HBM floor)"""
     import math
 
     g = engine.geom
     flops = executed = nbytes = 0.0
-    tm, tn = engine.tm, engine.tn
+    tn = engine.tn
     split = 3 if engine.filter_mode else 1
     esize = 4 if engine.filter_mode else 2  # bf16 operand (float32 pools: hi + lo copies)
     for li, s in enumerate(st.level_stats):
@@ -740,6 +741,7 @@ def sim_work(st, engine) -> dict:
         flops += float((2.0 * nl * nr).sum().item()) * g.r
         nbytes += float((nl + nr).sum().item()) * g.r * esize
         lv = engine.plan.levels[li]
+        tm = 512 if getattr(engine, "wide", None) and engine.wide[li] else engine.tm
         if engine.compact_from is not None and lv.height >= engine.compact_from:
             tiles = float((torch_ceil_div(nl, tm) * torch_ceil_div(nr, tn)).sum().item())
         else:

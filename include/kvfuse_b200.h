@@ -45,6 +45,8 @@ extern "C" {
 #define KVF_PATH_AUTO 0
 #define KVF_PATH_SIMT 1  /* CUDA-core similarity (f64 / f32 / bf16)           */
 #define KVF_PATH_TC 2    /* tcgen05 + TMEM + TMA similarity (bf16 pools only) */
+#define KVF_PATH_TC_WIDE 3 /* tcgen05, 512 x 256 tile per CTA pair (one TMEM
+                              accumulator; nsplit == 1, staged or direct rows) */
 
 /* Library identity and last error (thread-local). */
 const char* kvf_last_error(void);

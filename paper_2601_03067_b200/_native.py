@@ -26,6 +26,7 @@ KVF_ERR_CUDA = 4
 PATH_AUTO = 0
 PATH_SIMT = 1
 PATH_TC = 2
+PATH_TC_WIDE = 3  # tcgen05, 512 x 256 tile per CTA pair
 
 DT_F64, DT_F32, DT_BF16 = 0, 1, 2
 

@@ -46,6 +46,9 @@ constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quarter, each half of the colum
 static_assert(kTcPartialsPerTile == 2 * EPI_WARPS, "one moment slot per epilogue warp of the pair");
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*meta*/;
+// wide tile (256 A rows per CTA): 4 stages of 48 KB
+constexpr int SMEM_BYTES_WIDE = 4 * (2 * A_BYTES + B_BYTES) + 1024 + 8192;
+static_assert(SMEM_BYTES_WIDE <= 227 * 1024, "wide ring exceeds shared memory");
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // cluster smem address of CTA 0
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -248,6 +251,7 @@ constexpr uint32_t kSchedConsumers = 3 + 2 * EPI_WARPS;
 // the item to both CTAs' roles through a 4-deep shared-memory ring). TMEM
 // holds two 256-column accumulators, so the epilogue of tile k overlaps the
 // MMAs of tile k + 1 (tmem_full / tmem_empty barrier pair per buffer).
+template <int BMC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int64_t nU,
               const float* __restrict__ knorm, const uint8_t* __restrict__ fusable,
@@ -260,13 +264,23 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3,
               int nsplit, float* __restrict__ spart, int32_t* __restrict__ scnt,
               const __nv_bfloat16* __restrict__ pool) {
+  // BMC = A rows per CTA: 128 (pair tile 256 x 256, two TMEM accumulators, the epilogue of
+  // tile k overlaps the MMAs of tile k + 1) or 256 ("wide": pair tile 512 x 256, one
+  // accumulator filling TMEM; per k-step a CTA loads 32 KB of A + 16 KB of B for twice the
+  // MMAs, 171 instead of 128 FLOP per L2->SM byte -- the crossbar rate bounds the narrow tile)
+  constexpr bool WIDE = BMC == 256;
+  constexpr int STG = WIDE ? 4 : 6;            // ring stages (48 KB / 32 KB each)
+  constexpr int ABY = BMC * BK * 2;
+  constexpr int SBY = ABY + B_BYTES;
+  constexpr uint32_t NACC = WIDE ? 1 : 2;       // TMEM accumulators
+  if (WIDE) gathered = 0;  // gathered operands and split-K run on the narrow tile only
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ int split_last_sh;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint8_t* meta = smem + STAGES * STAGE_BYTES;
+  uint8_t* meta = smem + STG * SBY;
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(meta);
-  uint64_t* empty_bar = full_bar + STAGES;
-  uint64_t* tmem_full = empty_bar + STAGES;           // [2]
+  uint64_t* empty_bar = full_bar + STG;
+  uint64_t* tmem_full = empty_bar + STG;           // [2]
   uint64_t* tmem_empty = tmem_full + 2;               // [2], used on the leader
   uint64_t* sched_full = tmem_empty + 2;              // [SCHED_DEPTH]
   uint64_t* sched_empty = sched_full + SCHED_DEPTH;   // [SCHED_DEPTH], used on the leader
@@ -274,7 +288,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sched_rec + SCHED_DEPTH * kRec);
   // gathered rows on the LSU path (gathered == 2): per-CTA completion of a stage's
   // cp.async copies (both producer warps' lanes arrive on it)
-  uint64_t* full_loc = reinterpret_cast<uint64_t*>(meta + 448);  // [STAGES]
+  uint64_t* full_loc = reinterpret_cast<uint64_t*>(meta + 448);  // [STG]
   // epilogue column metadata, double-buffered by tile parity: [2][BN] each
   float* inv_j_b = reinterpret_cast<float*>(meta + 512);
   int32_t* colmin_b = reinterpret_cast<int32_t*>(meta + 512 + 8 * BN);
@@ -300,7 +314,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   const int lo_rows = (int)(g.L * g.NB);
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
+    for (int s = 0; s < STG; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
@@ -308,7 +322,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
     }
-    for (int s = 0; s < STAGES; ++s) mbar_init(&full_loc[s], 64);
+    for (int s = 0; s < STG; ++s) mbar_init(&full_loc[s], 64);
     for (int c = 0; c < 2 * BN; ++c) colmin_b[c] = kNone;
     for (int b = 0; b < SCHED_DEPTH; ++b) {
       mbar_init(&sched_full[b], 1);
@@ -355,7 +369,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int kr0 = (int)((int64_t)sk * nk_run / nsplit), kr1 = (int)((int64_t)(sk + 1) * nk_run / nsplit);
       const int layer = (int)(t.u / layer_div);
       const int head = g.head_mode ? (int)(t.u % g.h) : 0;
-      const int mi0 = t.i0 + (int)crank * BM;
+      const int mi0 = t.i0 + (int)crank * BMC;
       if (gathered == 2) {
         // LSU gather: warp 0 copies this CTA's 128 A rows, warp 2 its 128 B rows; a warp
         // instruction moves 4 rows x 128 B (lane = row (lane >> 3), 16-B chunk (lane & 7)),
@@ -377,11 +391,11 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         const uint32_t o0 = (uint32_t)(sub * 128 + ((ch ^ sub) * 16));
         const uint32_t o1 = (uint32_t)((sub + 4) * 128 + ((ch ^ (sub + 4)) * 16));
         for (int ks = 0; ks < nk; ++ks, ++kk) {
-          const int s = kk % STAGES;
-          const uint32_t ph = (kk / STAGES) & 1;
+          const int s = kk % STG;
+          const uint32_t ph = (kk / STG) & 1;
           if (lane == 0) mbar_wait(&empty_bar[s], ph ^ 1);
           __syncwarp();
-          const uint32_t tile = smem_u32(smem + s * STAGE_BYTES + pw * A_BYTES);
+          const uint32_t tile = smem_u32(smem + s * SBY + pw * ABY);
 #pragma unroll
           for (int i = 0; i < 32; ++i)  // rows 4i + sub: 8-row swizzle atoms at i/2 * 1024 B
             cp_async16(tile + (uint32_t)(i >> 1) * 1024u + ((i & 1) ? o1 : o0), base[i] + ks * 128);
@@ -404,15 +418,15 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
           rb[q] = layer * (int)g.NB + live[gb + t.pm + pb];
         }
         for (int ks = 0; ks < nk; ++ks, ++kk) {
-          const int s = kk % STAGES;
-          const uint32_t ph = (kk / STAGES) & 1;
+          const int s = kk % STG;
+          const uint32_t ph = (kk / STG) & 1;
           if (lane == 0) {
             mbar_wait(&empty_bar[s], ph ^ 1);
-            if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+            if (leader) mbar_expect_tx(&full_bar[s], 2 * SBY);
           }
           __syncwarp();
-          uint8_t* sa = smem + s * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
+          uint8_t* sa = smem + s * SBY;
+          uint8_t* sb = sa + ABY;
           tma_gather4_2sm(sa + lane * 4 * BK * 2, &tmap, &full_bar[s], ks * BK, ra);
           tma_gather4_2sm(sb + lane * 4 * BK * 2, &tmap, &full_bar[s], ks * BK, rb);
         }
@@ -424,8 +438,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
           (staged ? (int)(t.ul * g.NB) + t.pm + t.j0 : layer * g.NB + t.mid + t.j0) +
           (int)crank * BNH;
       for (int kr = kr0; kr < kr1; ++kr, ++kk) {
-        const int s = kk % STAGES;
-        const uint32_t ph = (kk / STAGES) & 1;
+        const int s = kk % STG;
+        const uint32_t ph = (kk / STG) & 1;
         mbar_wait(&empty_bar[s], ph ^ 1);
         const int part = kr / nk;  // split3 pass: 0 hi.hi, 1 hi.lo, 2 lo.hi
         const int ks = kr - part * nk;
@@ -435,10 +449,13 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         const int tok = g.head_mode ? rest : rest / g.h;
         // pool map: (d, h, t, rows); staged map: (64, r/64, 1, rows)
         const int c0 = staged ? 0 : dc * BK, c1 = staged ? ks : hh, c2 = staged ? 0 : tok;
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        uint8_t* sb = sa + A_BYTES;
-        if (leader) mbar_expect_tx(&full_bar[s], 2 * STAGE_BYTES);
+        uint8_t* sa = smem + s * SBY;
+        uint8_t* sb = sa + ABY;
+        if (leader) mbar_expect_tx(&full_bar[s], 2 * SBY);
         tma_load_4d_2sm(sa, &tmap, &full_bar[s], c0, c1, c2, rowA + (part == 2 ? lo_rows : 0));
+        if (WIDE)
+          tma_load_4d_2sm(sa + A_BYTES, &tmap, &full_bar[s], c0, c1, c2,
+                          rowA + BM + (part == 2 ? lo_rows : 0));
         tma_load_4d_2sm(sb, &tmap, &full_bar[s], c0, c1, c2, rowB + (part == 1 ? lo_rows : 0));
       }
     }
@@ -454,8 +471,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         mbar_arrive_cluster(&sched_empty[sl], 0);
         if (w < 0) break;
         for (int ks = 0; ks < nk; ++ks, ++kk) {
-          const int s = kk % STAGES;
-          mbar_wait(&full_loc[s], (kk / STAGES) & 1);
+          const int s = kk % STG;
+          mbar_wait(&full_loc[s], (kk / STG) & 1);
           fence_proxy_async_smem();
           mbar_arrive_cluster(&full_bar[s], 0);
         }
@@ -515,24 +532,27 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         mbar_arrive_cluster(&sched_empty[sl], 0);
         if (w < 0) break;
         const int nks = (int)((int64_t)(sk + 1) * nk_run / nsplit) - (int)((int64_t)sk * nk_run / nsplit);
-        const uint32_t acc = tc & 1;
-        mbar_wait_cluster(&tmem_empty[acc], ((tc >> 1) & 1) ^ 1);  // epilogue drained it
+        const uint32_t acc = tc % NACC;
+        mbar_wait_cluster(&tmem_empty[acc], ((tc / NACC) & 1) ^ 1);  // epilogue drained it
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dst = tmem_base + acc * BN;
+        const uint32_t dst = tmem_base + acc * BN;  // wide: rows half h at columns h * BN
         for (int ks = 0; ks < nks; ++ks, ++kk) {
-          const int s = kk % STAGES;
-          const uint32_t ph = (kk / STAGES) & 1;
+          const int s = kk % STG;
+          const uint32_t ph = (kk / STG) & 1;
           mbar_wait(&full_bar[s], ph);
           if (gathered == 2) {  // LSU gather: the peer's rows (relay above), then our own
             mbar_wait(&full_loc[s], ph);
             fence_proxy_async_smem();
           }
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint32_t sa = smem_u32(smem + s * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
+          const uint32_t sa = smem_u32(smem + s * SBY);
+          const uint32_t sb = sa + ABY;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_2sm(dst, sw128_desc(sa + k * 32), sw128_desc(sb + k * 32), (ks | k) != 0);
+          for (int hh = 0; hh < (WIDE ? 2 : 1); ++hh)
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_bf16_2sm(dst + hh * BN, sw128_desc(sa + hh * A_BYTES + k * 32),
+                            sw128_desc(sb + k * 32), (ks | k) != 0);
           umma_commit_2sm(&empty_bar[s]);
         }
         umma_commit_2sm(&tmem_full[acc]);
@@ -548,8 +568,12 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
     // level_stats), so no warp waits for another at the end of a tile.
     const int ew = warp - 4;
     const int quarter = ew & 3;           // TMEM lanes [32*quarter, 32*quarter + 32)
-    const int col0 = (ew >> 2) * (BN / 2);  // this warp's half of the columns
-    const int row = quarter * 32 + lane;
+    // narrow: two warps per lane quarter split the 256 columns; wide: they take the two
+    // 128-row halves of the CTA's 256 rows (TMEM columns [h * BN, h * BN + BN)), all columns
+    const int rh = WIDE ? (ew >> 2) : 0;
+    const int col0 = WIDE ? 0 : (ew >> 2) * (BN / 2);
+    const int col1 = WIDE ? BN : col0 + BN / 2;
+    const int row = rh * BM + quarter * 32 + lane;
     const int et = threadIdx.x - 128;
     constexpr int ET = 32 * EPI_WARPS;
     static_assert(ET >= BN, "one epilogue thread per column for the flush");
@@ -581,8 +605,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       double* pp = partials + (((int64_t)t.ul * nt + tile) * kTcPartialsPerTile + crank * EPI_WARPS + ew) * 5;
       const int64_t gb = t.u * g.NB;
       const int32_t* lv = live + gb;
-      const int mi0 = t.i0 + (int)crank * BM;
-      const int ni = max(0, min(BM, t.pm - t.pl - mi0));  // valid rows of this CTA
+      const int mi0 = t.i0 + (int)crank * BMC;
+      const int ni = max(0, min(BMC, t.pm - t.pl - mi0));  // valid rows of this CTA
       const int nj = min(BN, t.pr - t.pm - t.j0);
       for (int c = et; c < BN; c += ET) {  // column metadata
         const int64_t bj = gb + (c < nj ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
@@ -609,18 +633,19 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       flush(mb ^ 1);  // the previous tile's first matches (every warp is past it)
       prev_gb = gb;
 
-      const uint32_t acc = tc & 1;
-      mbar_wait(&tmem_full[acc], (tc >> 1) & 1);
+      const uint32_t acc = tc % NACC;
+      mbar_wait(&tmem_full[acc], (tc / NACC) & 1);
+      const uint32_t tcol = WIDE ? rh * BN : acc * BN;  // this warp's accumulator columns
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (nsplit > 1) {
         // this split's partial accumulator -> spart[(tile, split, CTA)][col][row]
         // (column-major: a warp's 32 rows are one 128-B line per column)
-        float* mine = spart + (((int64_t)w * nsplit + sk) * 2 + crank) * (int64_t)(BM * BN);
-        for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
+        float* mine = spart + (((int64_t)w * nsplit + sk) * 2 + crank) * (int64_t)(BMC * BN);
+        for (int c0 = col0; c0 < col1; c0 += 32) {
           uint32_t v[32];
-          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + tcol + c0, v);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) mine[(int64_t)(c0 + c) * BM + row] = __uint_as_float(v[c]);
+          for (int c = 0; c < 32; ++c) mine[(int64_t)(c0 + c) * BMC + row] = __uint_as_float(v[c]);
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
@@ -645,19 +670,19 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       // split partials in split order (bitwise reproducible)
       auto load_acc = [&](int c0, uint32_t (&v)[32]) {
         if (nsplit == 1) {
-          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN + c0, v);
+          tmem_ld32(tmem_base + ((uint32_t)(quarter * 32) << 16) + tcol + c0, v);
           return;
         }
-        const float* p0 = spart + ((int64_t)w * nsplit * 2 + crank) * (int64_t)(BM * BN) +
-                          (int64_t)c0 * BM + row;
+        const float* p0 = spart + ((int64_t)w * nsplit * 2 + crank) * (int64_t)(BMC * BN) +
+                          (int64_t)c0 * BMC + row;
         float a[32];
 #pragma unroll
         for (int c = 0; c < 32; ++c) a[c] = 0.f;
         for (int s = 0; s < nsplit; ++s) {  // 32 independent L2 loads in flight per split
-          const float* ps = p0 + (int64_t)s * 2 * BM * BN;
+          const float* ps = p0 + (int64_t)s * 2 * BMC * BN;
           float x[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) x[c] = __ldcg(ps + (int64_t)c * BM);
+          for (int c = 0; c < 32; ++c) x[c] = __ldcg(ps + (int64_t)c * BMC);
 #pragma unroll
           for (int c = 0; c < 32; ++c) a[c] += x[c];
         }
@@ -700,7 +725,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
           if (hit) atomicMin(&colmin[col], my_id);
         }
       };
-      for (int c0 = col0; c0 < col0 + BN / 2; c0 += 32) {
+      for (int c0 = col0; c0 < col1; c0 += 32) {
         uint32_t v[32];
         load_acc(c0, v);
         // columns of this chunk that take part (alive, fusable, inside the merge)
@@ -905,23 +930,28 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
   if (res != CUDA_SUCCESS) return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
+  const bool wide = a.wide != 0;
+  if (wide && (gathered || a.nsplit > 1)) return cudaErrorInvalidValue;
+  auto kern = wide ? sim_tc_kernel<2 * BM> : sim_tc_kernel<BM>;
+  const int smem_bytes = wide ? SMEM_BYTES_WIDE : SMEM_BYTES;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[wide]) {
     cudaError_t e =
-        cudaFuncSetAttribute(sim_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set[wide] = true;
   }
   float thr = (float)a.thr;
   if ((double)thr > a.thr) thr = nextafterf(thr, -INFINITY);  // (float)s > thr_f <=> s > thr
-  static int max_clusters = 0;
+  static int max_clusters_v[2] = {0, 0};
+  int& max_clusters = max_clusters_v[wide];
   if (max_clusters == 0) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2, 1, 1);
     cfg.blockDim = dim3(NTHREADS, 1, 1);
-    cfg.dynamicSmemBytes = SMEM_BYTES;
+    cfg.dynamicSmemBytes = smem_bytes;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, sim_tc_kernel, &cfg) != cudaSuccess || n <= 0) {
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n <= 0) {
       cudaGetLastError();
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
@@ -937,7 +967,7 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   int32_t* counter = work_counter(s);
   if (counter == nullptr) return cudaErrorMemoryAllocation;
   dim3 grid(2 * (unsigned)std::min<int64_t>(nwork, max_clusters), 1);
-  sim_tc_kernel<<<grid, NTHREADS, SMEM_BYTES, s>>>(
+  kern<<<grid, NTHREADS, smem_bytes, s>>>(
       tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
       a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? gmode : 0, split3 ? 1 : 0,

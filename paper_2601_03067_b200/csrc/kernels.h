@@ -51,6 +51,8 @@ struct SimArgs {
   int nsplit = 1;
   float* split_part = nullptr;
   int32_t* split_count = nullptr;
+  // wide tile (KVF_PATH_TC_WIDE): 512 x 256 per CTA pair (tiles of kTcTileMWide rows)
+  int wide = 0;
 };
 
 struct RescoreArgs {
@@ -78,6 +80,7 @@ cudaError_t launch_sim_simt(const SimArgs& a, cudaStream_t s);
 // tcgen05 path (bf16 only): one 256 x 256 tile per CTA pair (cta_group::2),
 // similarity partials written per CTA (2 slots per tile)
 constexpr int kTcTileM = 256;
+constexpr int kTcTileMWide = 512;
 constexpr int kTcTileN = 256;
 constexpr int kTcPartialsPerTile = 16;  // one moment slot per epilogue warp of the CTA pair
 bool tc_supported(const SimArgs& a, const char** why);

@@ -89,10 +89,11 @@ int kvf_sim_tile_shape(int dtype, int head_mode, int path, int* tile_m, int* til
                        int* partials_per_tile) {
   if (!tile_m || !tile_n || !partials_per_tile) return fail(KVF_ERR_INVALID, "null pointer");
   if (path == KVF_PATH_AUTO) path = dtype == BF16 ? KVF_PATH_TC : KVF_PATH_SIMT;
-  if (path == KVF_PATH_TC) {  // float32 pools run it on a bf16 operand copy (kvf_convert_rows)
+  if (path == KVF_PATH_TC || path == KVF_PATH_TC_WIDE) {
+    // float32 pools run it on a bf16 operand copy (kvf_convert_rows)
     if (dtype != BF16 && dtype != F32)
       return fail(KVF_ERR_INVALID, "tcgen05 path requires a bf16 or float32 pool");
-    *tile_m = kTcTileM;
+    *tile_m = path == KVF_PATH_TC_WIDE ? kTcTileMWide : kTcTileM;
     *tile_n = kTcTileN;
     *partials_per_tile = kTcPartialsPerTile;
     return KVF_OK;
@@ -162,6 +163,13 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
   if (filter && dtype != F32)
     return fail(KVF_ERR_INVALID, "a bf16 operand copy (filter) is for float32 pools");
   if (path == KVF_PATH_AUTO) path = (dtype == BF16 || filter) ? KVF_PATH_TC : KVF_PATH_SIMT;
+  if (path == KVF_PATH_TC_WIDE) {
+    if (nsplit != 1) return fail(KVF_ERR_INVALID, "the wide tcgen05 tile takes nsplit == 1");
+    if (live && !staged)
+      return fail(KVF_ERR_INVALID, "the wide tcgen05 tile takes staged (not gathered) compaction");
+    a.wide = 1;
+    path = KVF_PATH_TC;
+  }
   if (filter) {  // the tensor cores read the bf16 copy; re-scores read the fp32 pool
     if (path != KVF_PATH_TC) return fail(KVF_ERR_INVALID, "a filter copy needs the tcgen05 path");
     a.pool = filter;

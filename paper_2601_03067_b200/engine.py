@@ -213,8 +213,6 @@ class FusionEngine:
         self.pdev = _plan_device(plan, self.tm, self.tn, self.ppt, self.device)
         U, NB = geom.units, geom.NB
         dev = self.device
-        max_nt = max([lv["nt"] for lv in self.pdev.levels], default=1)
-        self.partials = torch.empty((U, max(max_nt * self.ppt, 1), 5), dtype=torch.float64, device=dev)
         # member counts / segments / absorber list of the current level
         self.level_ws = torch.zeros(int(N.lib().kvf_level_ws_ints(U * NB)), dtype=torch.int32,
                                     device=dev)
@@ -244,8 +242,10 @@ class FusionEngine:
         # split-K per level (tcgen05 path): few, long-K tiles (cfg1, CFF) spread over all SMs
         self.nsplit = [1] * len(self.pdev.levels)
         self.split_part = self.split_count = None
-        if path == N.PATH_TC and split:
+        pairs = 74
+        if path == N.PATH_TC:
             pairs = max(1, torch.cuda.get_device_properties(self.device).multi_processor_count // 2)
+        if path == N.PATH_TC and split:
             nk = geom.r // 64 * (3 if self.filter_mode else 1)
             need, tiles_max = 0, 0
             for li, lv in enumerate(self.pdev.levels):
@@ -263,6 +263,26 @@ class FusionEngine:
             if need:
                 self.split_part = torch.empty(need // 4, dtype=torch.float32, device=dev)
                 self.split_count = torch.zeros(2 * tiles_max, dtype=torch.int32, device=dev)
+        # wide tiles (512 x 256 per CTA pair, KVF_PATH_TC_WIDE) for the levels they fit: the
+        # narrow tile's 128 FLOP per L2->SM byte leaves the tensor pipe ~20% idle on the
+        # crossbar; the wide tile gives up the double-buffered TMEM accumulator for 171
+        self.wide = [False] * len(self.pdev.levels)
+        self.levels = list(self.pdev.levels)
+        if path == N.PATH_TC and geom.head_mode == 0 and compact_mode != "gathered":
+            wide_env = os.environ.get("KVF_SIM_WIDE", "auto")
+            tmw, _, _ = tile_shape(dtype, 0, N.PATH_TC_WIDE)
+            pdw = None
+            for li, lvp in enumerate(plan.levels):
+                if self.nsplit[li] != 1 or wide_env == "0" or not len(lvp.merges):
+                    continue
+                left_min = int((lvp.merges[:, 1] - lvp.merges[:, 0]).min())
+                if pdw is None:
+                    pdw = _plan_device(plan, tmw, self.tn, self.ppt, self.device)
+                if wide_env == "1" or (left_min >= tmw and pdw.levels[li]["nt"] * U >= 2 * pairs):
+                    self.wide[li] = True
+                    self.levels[li] = pdw.levels[li]
+        max_nt = max([lv["nt"] for lv in self.levels], default=1)
+        self.partials = torch.empty((U, max(max_nt * self.ppt, 1), 5), dtype=torch.float64, device=dev)
         self.shadow = self.sidx = self.scount = None
         self.shadow_cap = 0
         if self.exact:
@@ -365,7 +385,7 @@ class FusionEngine:
             self.sidx.fill_(-1)
             self.scount.zero_()
             st.shadow_count, st.shadow_cap = self.scount, self.shadow_cap
-        for li, lv in enumerate(self.pdev.levels):
+        for li, lv in enumerate(self.levels):
             nm, nt = lv["nm"], lv["nt"]
             stats = torch.empty((U, nm, 8), dtype=torch.float64, device=dev)
             samples = None
@@ -407,7 +427,8 @@ class FusionEngine:
                     N.ptr(self.rescore), self.rescore_cap, band,
                     N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx),
                     self.nsplit[li], N.ptr(self.split_part) if self.nsplit[li] > 1 else None,
-                    N.ptr(self.split_count) if self.nsplit[li] > 1 else None, self.path, sp,
+                    N.ptr(self.split_count) if self.nsplit[li] > 1 else None,
+                    N.PATH_TC_WIDE if self.wide[li] else self.path, sp,
                 )
                 if self.rescore_cap:
                     launches += 1

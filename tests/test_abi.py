@@ -53,6 +53,8 @@ def test_argument_errors_map_to_reference_exceptions():
     tm, tn, ppt = C.c_int(), C.c_int(), C.c_int()
     assert lib.kvf_sim_tile_shape(2, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
     assert (tm.value, tn.value, ppt.value) == (256, 256, 16)  # one moment slot per epilogue warp
+    assert lib.kvf_sim_tile_shape(2, 0, N.PATH_TC_WIDE, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
+    assert (tm.value, tn.value, ppt.value) == (512, 256, 16)
     # float32 pools run the tcgen05 path on a bf16 operand copy; float64 pools cannot
     assert lib.kvf_sim_tile_shape(1, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) == 0
     assert lib.kvf_sim_tile_shape(0, 0, N.PATH_TC, C.byref(tm), C.byref(tn), C.byref(ppt)) != 0
