@@ -314,7 +314,7 @@ class FusionEngine:
                 # staging holds the alive K rows of `stage_units` units at a time (compacted
                 # levels run in unit chunks): ~STAGE_BUDGET instead of a second full K pool
                 per_unit = NB * geom.r * 2
-                self.stage_units = max(1, min(U, STAGE_BUDGET // max(per_unit, 1)))
+                self.stage_units = max(1, min(U, stage_budget(self.device) // max(per_unit, 1)))
                 self.staged = torch.empty(self.stage_units * NB * geom.r, dtype=torch.bfloat16,
                                           device=dev)
 
@@ -478,7 +478,25 @@ class FusionEngine:
 
 COMPACT_BIG_MERGE = 65536  # blocks per merge (left + right)
 SPLIT_PART_BUDGET = 512 << 20  # bytes of split-K partials per engine
-STAGE_BUDGET = 4 << 30  # bytes of staged alive K rows (compacted levels, unit chunks)
+STAGE_BUDGET = 4 << 30  # minimum bytes of staged alive K rows (compacted levels, unit chunks)
+STAGE_FREE_FRACTION = 0.25  # ... raised to this share of the free device memory
+
+
+def stage_budget(device) -> int:
+    """Bytes for the staged alive K rows: STAGE_BUDGET, or a quarter of the free device
+    memory when that is larger (KVF_STAGE_BUDGET overrides). Every unit chunk of a
+    compacted level is one similarity launch with its own last-wave tail, so fewer, larger
+    chunks waste less (cfg2: 4 chunks of 8 layers at 4 GB, one chunk of 32 at 16 GB)."""
+    env = os.environ.get("KVF_STAGE_BUDGET")
+    if env:
+        return int(float(env) * (1 << 30))
+    budget = STAGE_BUDGET
+    try:
+        free, _ = torch.cuda.mem_get_info(device)
+        budget = max(budget, int(free * STAGE_FREE_FRACTION))
+    except Exception:
+        pass
+    return budget
 _TILE_PART_BYTES = 256 * 256 * 4  # one CTA pair's fp32 accumulator tile
 
 

@@ -21,7 +21,7 @@ def test_unit_chunks_bitwise(head_mode, monkeypatch):
     plan = bff_plan(B, p, None)
     states = []
     for budget in (1 << 40, 2 * B * p * geom.r * 2):  # everything at once / 2 units per chunk
-        monkeypatch.setattr(E, "STAGE_BUDGET", budget)
+        monkeypatch.setenv("KVF_STAGE_BUDGET", repr(budget / 2**30))  # GiB
         eng = E.FusionEngine(geom, plan, torch.bfloat16, Kt.device, compact_from=2, split=False)
         assert eng.stage_units == (geom.units if budget > 1 << 39 else 2)
         states.append(eng.run(Kt.clone().reshape(-1), Vt.clone().reshape(-1), 0.8, keep_samples=True))
