@@ -635,6 +635,10 @@ def ours_main(args):
                         "at eps 1e-9 (0 flips) and cfg1 at full shape vs the reference",
             },
             "sim_path": st_last.path_name,
+            "sim_tiles": {"wide_levels": [i + 1 for i, w in enumerate(engine.wide) if w],
+                          "compact_from_height": engine.compact_from,
+                          "stage_unit_chunks": -(-geom.units // engine.stage_units)
+                          if engine.compact_from is not None else None},
             "roofline": {
                 "kernel": sim_kernel,
                 "bound": "tensor" if engine.path == N.PATH_TC else "fp32",
