@@ -176,6 +176,195 @@ level_stats_kernel(int64_t u0, int64_t NB, int64_t n_total, const uint8_t* __res
   }
 }
 
+// ---------------------------------------------------------------------------
+// level statistics for few, large merges (the top levels: one CTA per merge
+// walked 262,144 blocks serially at cfg5, 10 ms for the top level). C CTAs per
+// (merge, unit) stride over the merge's range; the same outputs in five launches:
+//   ls_count    counters (integer-valued doubles, exact in any order) + member counts
+//   ls_segments absorber list and member segment bases (ascending inside a CTA step)
+//   ls_scatter  members appended with an atomic fill; moments of the CTA's share of
+//               the merge's tile partials, written over the share's first slot
+//   ls_sort     each absorber's member segment sorted ascending (the deterministic
+//               summation order of the one-CTA path)
+//   ls_moments  the C shares reduced in order
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ void merge_range(const int32_t* merges, int m, int& lb, int& mid, int& re) {
+  lb = merges[3 * m];
+  mid = merges[3 * m + 1];
+  re = merges[3 * m + 2];
+}
+// [a, b) = share c of C of the merge's partial slots [t0, t1)
+__device__ __forceinline__ void slot_share(int t0, int t1, int c, int C, int& a, int& b) {
+  const int64_t n = t1 - t0;
+  a = t0 + (int)(n * c / C);
+  b = t0 + (int)(n * (c + 1) / C);
+}
+}  // namespace
+
+__global__ void __launch_bounds__(LS_THREADS)
+ls_count_kernel(int64_t u0, int64_t NB, const uint8_t* __restrict__ fusable,
+                const uint8_t* __restrict__ alive, const int32_t* __restrict__ absorber,
+                const int32_t* __restrict__ merges, int nm, double* stats, int32_t* ws,
+                int64_t n_total) {
+  __shared__ double red[32];
+  LevelWs W(ws, n_total);
+  const int C = gridDim.x, c = blockIdx.x, m = blockIdx.y;
+  const int64_t ul = blockIdx.z, gb = (u0 + ul) * NB;
+  int lb, mid, re;
+  merge_range(merges, m, lb, mid, re);
+  double nl = 0, nr = 0, nf = 0;
+  for (int i = lb + c * LS_THREADS + threadIdx.x; i < re; i += C * LS_THREADS) {
+    const bool al = alive[gb + i], fu = fusable[gb + i];
+    if (i < mid) {
+      nl += (al && fu) ? 1.0 : 0.0;
+    } else {
+      nr += (al && fu) ? 1.0 : 0.0;
+      const int32_t a = absorber[gb + i];
+      if (al && a != kNone) {
+        nf += 1.0;
+        atomicAdd(&W.mcnt[gb + a], 1);
+      }
+    }
+  }
+  nl = block_sum(nl, red);
+  nr = block_sum(nr, red);
+  nf = block_sum(nf, red);
+  if (threadIdx.x == 0) {
+    double* o = stats + (ul * nm + m) * 8;
+    atomicAdd(o + 0, nl);
+    atomicAdd(o + 1, nr);
+    atomicAdd(o + 2, nf);
+  }
+}
+
+__global__ void __launch_bounds__(LS_THREADS)
+ls_segments_kernel(int64_t u0, int64_t NB, const int32_t* __restrict__ merges, int32_t* ws,
+                   int64_t n_total) {
+  __shared__ int wsum[LS_WARPS];
+  __shared__ int tot_c, tot_f, cbase, lbase;
+  LevelWs W(ws, n_total);
+  const int C = gridDim.x, c = blockIdx.x, m = blockIdx.y;
+  const int64_t gb = (u0 + blockIdx.z) * NB;
+  int lb, mid, re;
+  merge_range(merges, m, lb, mid, re);
+  for (int c0 = lb + c * LS_THREADS; c0 < mid; c0 += C * LS_THREADS) {
+    const int i = c0 + threadIdx.x;
+    const int n = i < mid ? W.mcnt[gb + i] : 0;
+    const int oc = block_excl_scan(n, wsum, &tot_c);
+    const int of = block_excl_scan(n > 0 ? 1 : 0, wsum, &tot_f);
+    if (tot_f == 0) continue;  // block-uniform
+    if (threadIdx.x == 0) {
+      cbase = atomicAdd(W.cursor, tot_c);
+      lbase = atomicAdd(W.count, tot_f);
+    }
+    __syncthreads();
+    if (n > 0) {
+      W.mstart[gb + i] = cbase + oc;
+      W.list[lbase + of] = (int32_t)(gb + i);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(LS_THREADS)
+ls_scatter_kernel(int64_t u0, int64_t NB, const uint8_t* __restrict__ alive,
+                  const int32_t* __restrict__ absorber, const int32_t* __restrict__ merges,
+                  const int32_t* __restrict__ tile_off, int nt, double* partials, int32_t* ws,
+                  int64_t n_total) {
+  __shared__ double red[32];
+  __shared__ double smn[LS_WARPS], smx[LS_WARPS];
+  LevelWs W(ws, n_total);
+  const int C = gridDim.x, c = blockIdx.x, m = blockIdx.y;
+  const int64_t ul = blockIdx.z, gb = (u0 + ul) * NB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int lb, mid, re;
+  merge_range(merges, m, lb, mid, re);
+  for (int j = mid + c * LS_THREADS + threadIdx.x; j < re; j += C * LS_THREADS) {
+    const int32_t a = absorber[gb + j];
+    if (a != kNone && alive[gb + j]) {
+      const int pos = atomicAdd(&W.mfill[gb + a], 1);
+      W.members[W.mstart[gb + a] + pos] = j;
+    }
+  }
+  // this CTA's share of the merge's tile partials (fixed range, fixed order)
+  int a0, a1;
+  slot_share(tile_off[m], tile_off[m + 1], c, C, a0, a1);
+  double* pb = partials + ul * (int64_t)nt * 5;
+  double cn = 0, s1 = 0, s2 = 0, mn = INFINITY, mx = -INFINITY;
+  for (int tt = a0 + threadIdx.x; tt < a1; tt += blockDim.x) {
+    const double* q = pb + (int64_t)tt * 5;
+    cn += q[0];
+    s1 += q[1];
+    s2 += q[2];
+    mn = fmin(mn, q[3]);
+    mx = fmax(mx, q[4]);
+  }
+  cn = block_sum(cn, red);
+  s1 = block_sum(s1, red);
+  s2 = block_sum(s2, red);
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    smn[warp] = mn;
+    smx[warp] = mx;
+  }
+  __syncthreads();  // every thread has read its share before the first slot is overwritten
+  if (threadIdx.x == 0 && a1 > a0) {
+    for (int w = 1; w < LS_WARPS; ++w) {
+      mn = fmin(mn, smn[w]);
+      mx = fmax(mx, smx[w]);
+    }
+    double* o = pb + (int64_t)a0 * 5;
+    o[0] = cn; o[1] = s1; o[2] = s2; o[3] = mn; o[4] = mx;
+  }
+}
+
+__global__ void ls_sort_kernel(int32_t* ws, int64_t n_total) {
+  LevelWs W(ws, n_total);
+  const int n_items = *W.count;
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < n_items; it += gridDim.x * blockDim.x) {
+    const int64_t gid = W.list[it];
+    int32_t* seg = W.members + W.mstart[gid];
+    const int n = W.mcnt[gid];
+    for (int x = 1; x < n; ++x) {  // insertion sort: segments hold a few members
+      const int32_t v = seg[x];
+      int y = x - 1;
+      while (y >= 0 && seg[y] > v) {
+        seg[y + 1] = seg[y];
+        --y;
+      }
+      seg[y + 1] = v;
+    }
+  }
+}
+
+__global__ void ls_moments_kernel(const int32_t* __restrict__ tile_off, int nt, int nm, int C,
+                                  const double* __restrict__ partials, double* stats) {
+  const int m = blockIdx.x;
+  const int64_t ul = blockIdx.y;
+  if (threadIdx.x != 0) return;
+  const double* pb = partials + ul * (int64_t)nt * 5;
+  double cn = 0, s1 = 0, s2 = 0, mn = INFINITY, mx = -INFINITY;
+  for (int c = 0; c < C; ++c) {
+    int a0, a1;
+    slot_share(tile_off[m], tile_off[m + 1], c, C, a0, a1);
+    if (a1 <= a0) continue;
+    const double* q = pb + (int64_t)a0 * 5;
+    cn += q[0];
+    s1 += q[1];
+    s2 += q[2];
+    mn = fmin(mn, q[3]);
+    mx = fmax(mx, q[4]);
+  }
+  double* o = stats + (ul * nm + m) * 8;
+  o[3] = cn; o[4] = s1; o[5] = s2;
+  o[6] = cn > 0 ? mn : 0.0;
+  o[7] = cn > 0 ? mx : 0.0;
+}
+
 cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_total,
                                const uint8_t* fusable, const uint8_t* alive,
                                const int32_t* absorber, const int32_t* merges, int nm,
@@ -185,6 +374,28 @@ cudaError_t launch_level_stats(int64_t u0, int64_t nU, int64_t NB, int64_t n_tot
   // count, cursor, merge item fetch counter
   cudaError_t e = cudaMemsetAsync(W.count, 0, 3 * sizeof(int32_t), s);
   if (e != cudaSuccess || nm == 0 || nU == 0) return e;
+  // few, large merges (fewer CTAs than two waves, >= 8192 blocks per merge on average):
+  // C CTAs per merge (KVF_LS_CHUNKED=0/1 forces the one-CTA / chunked path)
+  const char* force = getenv("KVF_LS_CHUNKED");
+  const int64_t per_merge = NB / nm;
+  bool chunked = nm * nU < 2 * 148 && per_merge >= 8192;
+  if (force) chunked = force[0] == '1';
+  if (chunked) {
+    int C = (int)std::max<int64_t>(1, std::min<int64_t>((2 * 148 + nm * nU - 1) / (nm * nU),
+                                                         std::max<int64_t>(1, per_merge / 2048)));
+    dim3 g3(C, nm, (unsigned)nU);
+    e = cudaMemsetAsync(stats, 0, sizeof(double) * 8 * nm * nU, s);
+    if (e != cudaSuccess) return e;
+    double* part = const_cast<double*>(partials);
+    ls_count_kernel<<<g3, LS_THREADS, 0, s>>>(u0, NB, fusable, alive, absorber, merges, nm, stats,
+                                              level_ws, n_total);
+    ls_segments_kernel<<<g3, LS_THREADS, 0, s>>>(u0, NB, merges, level_ws, n_total);
+    ls_scatter_kernel<<<g3, LS_THREADS, 0, s>>>(u0, NB, alive, absorber, merges, tile_off, nt, part,
+                                                level_ws, n_total);
+    ls_sort_kernel<<<148, 256, 0, s>>>(level_ws, n_total);
+    ls_moments_kernel<<<dim3(nm, (unsigned)nU), 32, 0, s>>>(tile_off, nt, nm, C, part, stats);
+    return cudaGetLastError();
+  }
   dim3 grid(nm, (unsigned)nU);
   level_stats_kernel<<<grid, LS_THREADS, 0, s>>>(u0, NB, n_total, fusable, alive, absorber,
                                                  merges, nm, tile_off, nt, partials, stats,
