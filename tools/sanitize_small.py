@@ -19,6 +19,16 @@ for hm in ("folded", "per_head"):
     outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8, head_mode=hm), keep_samples=True)
     torch.cuda.synchronize()
     print("bf16", hm, sum(o.report.blocks_before for o in outs) / sum(o.report.blocks_after for o in outs))
+# wide similarity tiles (512 x 256 per CTA pair) + chunked level statistics, staged compaction
+os.environ["KVF_SIM_WIDE"] = "1"
+os.environ["KVF_LS_CHUNKED"] = "1"
+for dt in (torch.bfloat16, torch.float32):
+    Kt, Vt = synthetic_kv(2, 16, 96, 16, 8, 128, dtype=dt, seed=10)
+    cache = K.PagedKvCache(K.CacheDims(B=16, p=96, t=16, h=8, d=128, L=2), Kt, Vt)
+    outs = K.fuse_batch(cache, K.FusionConfig(threshold=0.8), keep_samples=dt == torch.float32)
+    torch.cuda.synchronize()
+    print("wide + chunked stats", dt, outs[0].report.compression_ratio)
+del os.environ["KVF_SIM_WIDE"], os.environ["KVF_LS_CHUNKED"]
 # compacted levels with the alive rows gathered from the pool (cp.async + peer relay)
 from paper_2601_03067_b200 import _native as N  # noqa: E402
 from paper_2601_03067_b200.engine import FusionEngine, Geometry  # noqa: E402
