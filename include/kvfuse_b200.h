@@ -47,6 +47,12 @@ extern "C" {
 #define KVF_PATH_TC 2    /* tcgen05 + TMEM + TMA similarity (bf16 pools only) */
 #define KVF_PATH_TC_WIDE 3 /* tcgen05, 512 x 256 tile per CTA pair (one TMEM
                               accumulator; nsplit == 1, staged or direct rows) */
+/* OR-ed into kvf_similarity_select's path (KVF_PATH_TC, bf16 pool, folded units,
+ * nsplit == 1, direct rows): the launch computes the key norm of every row it streams
+ * from the shared-memory stages (the tree's first level, where each block is an operand
+ * row of exactly one tile) and writes knorm and fusable = (knorm > 0) itself -- replaces
+ * the K pass of kvf_block_norms (core.py:115-119) with no extra HBM read. */
+#define KVF_SIM_WRITE_NORMS 0x100
 
 /* Library identity and last error (thread-local). */
 const char* kvf_last_error(void);
@@ -64,7 +70,8 @@ int kvf_block_norms(const void* pool, int dtype, int64_t L, int64_t NB, int t,
 
 /* Fusion state for U units (replaces _Engine.__init__, fusion.py:208-228, and
  * BlockTable.identity, core.py:191-201): fusable = knorm > 0, alive = 1,
- * absorber = NONE, table = identity, refcount = 1. */
+ * absorber = NONE, table = identity, refcount = 1. knorm == NULL leaves fusable
+ * to the level-1 similarity launch with KVF_SIM_WRITE_NORMS. */
 int kvf_state_init(int dtype, int64_t U, int64_t NB, const void* knorm,
                    uint8_t* fusable, uint8_t* alive, int32_t* absorber,
                    int32_t* table, int32_t* refcount, void* stream);

@@ -27,6 +27,7 @@ PATH_AUTO = 0
 PATH_SIMT = 1
 PATH_TC = 2
 PATH_TC_WIDE = 3  # tcgen05, 512 x 256 tile per CTA pair
+SIM_WRITE_NORMS = 0x100  # OR-ed into the path: level-1 launch computes the key norms
 
 DT_F64, DT_F32, DT_BF16 = 0, 1, 2
 

@@ -208,7 +208,7 @@ __global__ void state_init_kernel(int64_t U, int64_t NB, const A* __restrict__ k
   const int64_t n = U * NB;
   for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n;
        x += (int64_t)gridDim.x * blockDim.x) {
-    fusable[x] = knorm[x] > A(0) ? 1 : 0;
+    if (knorm) fusable[x] = knorm[x] > A(0) ? 1 : 0;
     alive[x] = 1;
     absorber[x] = kNone;
     table[x] = (int32_t)(x % NB);

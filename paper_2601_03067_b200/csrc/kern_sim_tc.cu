@@ -45,9 +45,10 @@ constexpr int TMEM_COLS = 512;  // two 256-column accumulators
 constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quarter, each half of the columns
 static_assert(kTcPartialsPerTile == 2 * EPI_WARPS, "one moment slot per epilogue warp of the pair");
 constexpr int NTHREADS = 128 + 32 * EPI_WARPS;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 8192 /*meta*/;
+constexpr int META_BYTES = 12288;  // barriers, work records, epilogue / norm metadata
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + META_BYTES;
 // wide tile (256 A rows per CTA): 4 stages of 48 KB
-constexpr int SMEM_BYTES_WIDE = 4 * (2 * A_BYTES + B_BYTES) + 1024 + 8192;
+constexpr int SMEM_BYTES_WIDE = 4 * (2 * A_BYTES + B_BYTES) + 1024 + META_BYTES;
 static_assert(SMEM_BYTES_WIDE <= 227 * 1024, "wide ring exceeds shared memory");
 constexpr uint32_t kPeerMask = 0xFEFFFFFFu;  // cluster smem address of CTA 0
 
@@ -254,7 +255,7 @@ constexpr uint32_t kSchedConsumers = 3 + 2 * EPI_WARPS;
 template <int BMC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NTHREADS, 1)
 sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int64_t nU,
-              const float* __restrict__ knorm, const uint8_t* __restrict__ fusable,
+              float* __restrict__ knorm, uint8_t* __restrict__ fusable,
               const uint8_t* __restrict__ alive, int32_t* __restrict__ absorber,
               const int32_t* __restrict__ merges, const int32_t* __restrict__ tiles, int nt,
               float thr, double* __restrict__ partials, double* __restrict__ samples,
@@ -263,7 +264,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
               float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3,
               int nsplit, float* __restrict__ spart, int32_t* __restrict__ scnt,
-              const __nv_bfloat16* __restrict__ pool) {
+              const __nv_bfloat16* __restrict__ pool, int fnorm) {
   // BMC = A rows per CTA: 128 (pair tile 256 x 256, two TMEM accumulators, the epilogue of
   // tile k overlaps the MMAs of tile k + 1) or 256 ("wide": pair tile 512 x 256, one
   // accumulator filling TMEM; per k-step a CTA loads 32 KB of A + 16 KB of B for twice the
@@ -294,6 +295,17 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   int32_t* colmin_b = reinterpret_cast<int32_t*>(meta + 512 + 8 * BN);
   int32_t* colid_b = reinterpret_cast<int32_t*>(meta + 512 + 16 * BN);  // block ids
   uint8_t* ok_j_b = meta + 512 + 24 * BN;
+  // fused key norms (fnorm, level 1): per-stage "MMA done" barriers in both CTAs (the norm
+  // warps copy a stage's rows to registers after the MMAs read it -- the MMA commit is the
+  // one completion signal the peer CTA receives for its own rows -- and release it next to
+  // the commit; relaying the leader's full barrier to the peer instead measured slower:
+  // cluster-scope acquires invalidate L1 on every stage), norms-ready barriers by tile
+  // parity, and the tile's row / column norms ([2][BM] A rows, [2][BN] B rows of the pair)
+  uint64_t* mma_done = reinterpret_cast<uint64_t*>(meta + 7168);  // [STG]
+  uint64_t* norm_ready = mma_done + 8;                              // [2]
+  float* anorm_b = reinterpret_cast<float*>(meta + 8192);
+  float* bnorm_b = anorm_b + 2 * BM;
+  if (WIDE) fnorm = 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
@@ -316,8 +328,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   if (threadIdx.x == 0) {
     for (int s = 0; s < STG; ++s) {
       mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
+      mbar_init(&empty_bar[s], fnorm ? 1 + EPI_WARPS : 1);  // MMA commit (+ the norm warps)
+      mbar_init(&mma_done[s], 1);
     }
+    for (int b = 0; b < 2; ++b) mbar_init(&norm_ready[b], 2 * EPI_WARPS);  // both CTAs
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tmem_full[b], 1);
       mbar_init(&tmem_empty[b], 2 * EPI_WARPS);  // epilogue warps x 2 CTAs
@@ -554,6 +568,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               umma_bf16_2sm(dst + hh * BN, sw128_desc(sa + hh * A_BYTES + k * 32),
                             sw128_desc(sb + k * 32), (ks | k) != 0);
           umma_commit_2sm(&empty_bar[s]);
+          if (fnorm) umma_commit_2sm(&mma_done[s]);  // the stage is readable by the norm warps
         }
         umma_commit_2sm(&tmem_full[acc]);
         ++tc;
@@ -578,6 +593,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
     constexpr int ET = 32 * EPI_WARPS;
     static_assert(ET >= BN, "one epilogue thread per column for the flush");
     uint32_t tc = 0;
+    uint32_t kn = 0;  // fnorm: ring position of the norm pass (the MMA warp's k-step sequence)
     int64_t prev_gb = -1;  // unit base of the tile whose minima are pending
     auto flush = [&](int buf) {  // thread et owns column et of buffer buf
       if (et < BN && prev_gb >= 0) {
@@ -608,11 +624,77 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int mi0 = t.i0 + (int)crank * BMC;
       const int ni = max(0, min(BMC, t.pm - t.pl - mi0));  // valid rows of this CTA
       const int nj = min(BN, t.pr - t.pm - t.j0);
+      if (fnorm) {
+        // Key norms of the rows this CTA streams (level 1: every block is an operand row of
+        // exactly one tile), read from the ring after the MMAs: thread et takes A row et
+        // or B row et - BM; 8-element fp32 partials of exact bf16 squares summed in float64,
+        // as block_norms_flat_kernel does. The stage is released to the producer by the MMA
+        // commit plus one arrival per norm warp.
+        const int nrow = et & (BM - 1);
+        const bool isA = et < BM;
+        const uint32_t roff = (isA ? 0u : (uint32_t)A_BYTES) + (uint32_t)nrow * 128u;
+        double nacc8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // one chain per chunk slot
+        for (int ks = 0; ks < nk_run; ++ks, ++kn) {
+          const int s = kn % STG;
+          if (lane == 0) mbar_wait(&mma_done[s], (kn / STG) & 1);  // one poller per warp
+          __syncwarp();
+          const uint32_t rp = smem_u32(smem + s * SBY) + roff;
+          uint4 q[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c)  // 16-B chunk c of the row sits at chunk c ^ (row % 8)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(q[c].x), "=r"(q[c].y), "=r"(q[c].z), "=r"(q[c].w)
+                         : "r"(rp + ((uint32_t)(c ^ (nrow & 7)) << 4))
+                         : "memory");
+          __syncwarp();  // the row is in registers: release the stage before the math
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty_bar[s])) : "memory");
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const __nv_bfloat162* p2 = reinterpret_cast<const __nv_bfloat162*>(&q[c]);
+            float a = 0.f;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(p2[e]);
+              a = fmaf(f.x, f.x, a);
+              a = fmaf(f.y, f.y, a);
+            }
+            nacc8[c] += a;  // independent float64 chains (the sum is exact in practice)
+          }
+        }
+        const double nacc = ((nacc8[0] + nacc8[1]) + (nacc8[2] + nacc8[3])) +
+                            ((nacc8[4] + nacc8[5]) + (nacc8[6] + nacc8[7]));
+        const float nv = (float)sqrt(nacc);
+        if (isA) {
+          anorm_b[mb * BM + nrow] = nv;
+          if (nrow < ni) {
+            knorm[gb + t.lb + mi0 + nrow] = nv;
+            fusable[gb + t.lb + mi0 + nrow] = nv > 0.f ? 1 : 0;
+          }
+        } else {
+          const int cg = (int)crank * BNH + nrow;  // column of the pair tile
+          bnorm_b[mb * BN + cg] = nv;
+          asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(cluster_addr(&bnorm_b[mb * BN + cg], crank ^ 1)),
+                       "f"(nv)
+                       : "memory");
+          if (cg < nj) {
+            knorm[gb + t.mid + t.j0 + cg] = nv;
+            fusable[gb + t.mid + t.j0 + cg] = nv > 0.f ? 1 : 0;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive_cluster(&norm_ready[mb], 0);
+          mbar_arrive_cluster(&norm_ready[mb], 1);
+        }
+        mbar_wait_cluster(&norm_ready[mb], (tc >> 1) & 1);  // both CTAs' norms of this tile
+      }
       for (int c = et; c < BN; c += ET) {  // column metadata
         const int64_t bj = gb + (c < nj ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
         // independent loads (one round trip), combined afterwards
-        const uint8_t al = alive[bj], fu = fusable[bj];
-        const float nk = knorm[bj];
+        const uint8_t al = alive[bj];
+        const float nk = fnorm ? bnorm_b[mb * BN + c] : knorm[bj];
+        const uint8_t fu = fnorm ? (nk > 0.f ? 1 : 0) : fusable[bj];
         const bool ok = c < nj && al && fu;
         colid[c] = (int32_t)(bj - gb);
         const float nv = ok ? nk : 0.f;
@@ -621,8 +703,9 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       }
       const int32_t my_id = row < ni ? (staged ? lv[t.pl + mi0 + row] : t.lb + mi0 + row) : 0;
       const int64_t bi = gb + my_id;
-      const uint8_t al_i = alive[bi], fu_i = fusable[bi];
-      const float nk_i = knorm[bi];
+      const uint8_t al_i = alive[bi];
+      const float nk_i = fnorm ? anorm_b[mb * BM + row] : knorm[bi];
+      const uint8_t fu_i = fnorm ? (nk_i > 0.f ? 1 : 0) : fusable[bi];
       const bool ok_i = row < ni && al_i && fu_i;
       const float ni_v = ok_i ? nk_i : 0.f;
       const float inv_i = ni_v > 0.f ? 1.f / ni_v : 0.f;
@@ -932,6 +1015,8 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   if (res != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const bool wide = a.wide != 0;
   if (wide && (gathered || a.nsplit > 1)) return cudaErrorInvalidValue;
+  if (a.write_norms && (wide || compact || a.nsplit > 1 || split3 || g.head_mode))
+    return cudaErrorInvalidValue;
   auto kern = wide ? sim_tc_kernel<2 * BM> : sim_tc_kernel<BM>;
   const int smem_bytes = wide ? SMEM_BYTES_WIDE : SMEM_BYTES;
   static bool attr_set[2] = {false, false};
@@ -968,10 +1053,11 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   if (counter == nullptr) return cudaErrorMemoryAllocation;
   dim3 grid(2 * (unsigned)std::min<int64_t>(nwork, max_clusters), 1);
   kern<<<grid, NTHREADS, smem_bytes, s>>>(
-      tmap, g, a.u0, a.nU, (const float*)a.knorm, a.fusable, a.alive, a.absorber, a.merges, a.tiles,
+      tmap, g, a.u0, a.nU, (float*)const_cast<void*>(a.knorm), const_cast<uint8_t*>(a.fusable), a.alive,
+      a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
       a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? gmode : 0, split3 ? 1 : 0,
-      nsplit, a.split_part, a.split_count, (const __nv_bfloat16*)a.pool);
+      nsplit, a.split_part, a.split_count, (const __nv_bfloat16*)a.pool, a.write_norms && !wide ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -53,6 +53,9 @@ struct SimArgs {
   int32_t* split_count = nullptr;
   // wide tile (KVF_PATH_TC_WIDE): 512 x 256 per CTA pair (tiles of kTcTileMWide rows)
   int wide = 0;
+  // level 1 only: the launch computes the key norm of every streamed row (knorm written,
+  // fusable = knorm > 0) instead of reading them (KVF_SIM_WRITE_NORMS)
+  int write_norms = 0;
 };
 
 struct RescoreArgs {

@@ -162,6 +162,14 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
   a.split_count = split_count;
   if (filter && dtype != F32)
     return fail(KVF_ERR_INVALID, "a bf16 operand copy (filter) is for float32 pools");
+  if (path & KVF_SIM_WRITE_NORMS) {
+    path &= ~KVF_SIM_WRITE_NORMS;
+    if (path != KVF_PATH_TC || dtype != BF16 || head_mode || nsplit != 1 || live || filter)
+      return fail(KVF_ERR_INVALID,
+                  "KVF_SIM_WRITE_NORMS needs the narrow tcgen05 tile, a bf16 pool, folded units, "
+                  "nsplit == 1 and direct rows");
+    a.write_norms = 1;
+  }
   if (path == KVF_PATH_AUTO) path = (dtype == BF16 || filter) ? KVF_PATH_TC : KVF_PATH_SIMT;
   if (path == KVF_PATH_TC_WIDE) {
     if (nsplit != 1) return fail(KVF_ERR_INVALID, "the wide tcgen05 tile takes nsplit == 1");

@@ -16,6 +16,7 @@ _fuse_layer (fusion.py:290-336), restated level-synchronously.
 
 from __future__ import annotations
 
+import contextlib
 import os
 
 from dataclasses import dataclass, field
@@ -283,6 +284,20 @@ class FusionEngine:
                     self.levels[li] = pdw.levels[li]
         max_nt = max([lv["nt"] for lv in self.levels], default=1)
         self.partials = torch.empty((U, max(max_nt * self.ppt, 1), 5), dtype=torch.float64, device=dev)
+        # key norms fused into the first level's similarity launch (KVF_SIM_WRITE_NORMS):
+        # every block is an operand row of exactly one level-1 tile when every row takes part
+        # in a level-1 merge whose sides fit one narrow tile; saves the K pass of the norms
+        # (17 GB read per cfg2 step)
+        self.fuse_knorm = False
+        if (path == N.PATH_TC and dtype == torch.bfloat16 and geom.head_mode == 0 and plan.levels
+                and os.environ.get("KVF_FUSE_KNORM", "1") != "0"):
+            lv0 = plan.levels[0]
+            m0 = lv0.merges
+            compact0 = compact_from is not None and lv0.height >= compact_from
+            self.fuse_knorm = bool(
+                len(m0) and self.nsplit[0] == 1 and not self.wide[0] and not compact0
+                and (lv0.row_merge >= 0).all()
+                and int((m0[:, 1] - m0[:, 0]).max()) <= self.tm and int((m0[:, 2] - m0[:, 1]).max()) <= self.tn)
         self.shadow = self.sidx = self.scount = None
         self.shadow_cap = 0
         if self.exact:
@@ -353,10 +368,18 @@ class FusionEngine:
         U, NB = g.units, g.NB
         acc = acc_dtype(self.dtype)
         launches = 0
-        knorm = block_norms(pool_k, g, stream)
+        fuse_knorm = self.fuse_knorm and orig_knorm is None
+        if fuse_knorm:  # written by the level-1 similarity launch
+            knorm = torch.empty((U, NB), dtype=torch.float32, device=dev)
+        else:
+            knorm = block_norms(pool_k, g, stream)
+            launches += 1
         vnorm = block_norms(pool_v, g, stream)
-        launches += 2
-        oknorm = knorm.clone() if orig_knorm is None else orig_knorm.reshape(U, NB).to(acc)
+        launches += 1
+        if fuse_knorm:
+            oknorm = torch.empty_like(knorm)  # copied from knorm after the level-1 launch
+        else:
+            oknorm = knorm.clone() if orig_knorm is None else orig_knorm.reshape(U, NB).to(acc)
         ovnorm = vnorm.clone() if orig_vnorm is None else orig_vnorm.reshape(U, NB).to(acc)
         fusable = torch.empty((U, NB), dtype=torch.uint8, device=dev)
         alive_t = torch.empty((U, NB), dtype=torch.uint8, device=dev) if alive is None else alive
@@ -364,7 +387,7 @@ class FusionEngine:
         table_t = torch.empty((U, NB), dtype=torch.int32, device=dev) if table is None else table
         ref_t = torch.empty((U, NB), dtype=torch.int32, device=dev) if refcount is None else refcount
         N.call(
-            "kvf_state_init", dt, U, NB, N.ptr(oknorm), N.ptr(fusable), N.ptr(alive_t),
+            "kvf_state_init", dt, U, NB, None if fuse_knorm else N.ptr(oknorm), N.ptr(fusable), N.ptr(alive_t),
             N.ptr(absorber), N.ptr(table_t), N.ptr(ref_t), sp,
         )
         launches += 1
@@ -428,7 +451,8 @@ class FusionEngine:
                     N.ptr(self.filter), N.ptr(self.shadow), N.ptr(self.sidx),
                     self.nsplit[li], N.ptr(self.split_part) if self.nsplit[li] > 1 else None,
                     N.ptr(self.split_count) if self.nsplit[li] > 1 else None,
-                    N.PATH_TC_WIDE if self.wide[li] else self.path, sp,
+                    (N.PATH_TC_WIDE if self.wide[li] else self.path)
+                    | (N.SIM_WRITE_NORMS if fuse_knorm and li == 0 else 0), sp,
                 )
                 if self.rescore_cap:
                     launches += 1
@@ -438,6 +462,9 @@ class FusionEngine:
                 if time_sim:
                     e1.record(stream)
                     st.sim_events.append((e0, e1, li))
+            if fuse_knorm and li == 0:  # original key norms = the freshly written ones
+                with torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext():
+                    oknorm.copy_(knorm)
             N.call(
                 "kvf_level_stats", 0, U, U, NB, N.ptr(fusable), N.ptr(alive_t), N.ptr(absorber),
                 N.ptr(lv["merges"]), nm, N.ptr(lv["tile_off_p"]), nt * self.ppt,
