@@ -636,6 +636,8 @@ def ours_main(args):
             },
             "sim_path": st_last.path_name,
             "sim_tiles": {"wide_levels": [i + 1 for i, w in enumerate(engine.wide) if w],
+                          "paired_levels": [i + 1 for i, w in enumerate(engine.paired) if w],
+                          "fused_key_norms": engine.fuse_knorm,
                           "compact_from_height": engine.compact_from,
                           "stage_unit_chunks": -(-geom.units // engine.stage_units)
                           if engine.compact_from is not None else None},
@@ -748,6 +750,8 @@ def sim_work(st, engine) -> dict:
         tm = 512 if getattr(engine, "wide", None) and engine.wide[li] else engine.tm
         if engine.compact_from is not None and lv.height >= engine.compact_from:
             tiles = float((torch_ceil_div(nl, tm) * torch_ceil_div(nr, tn)).sum().item())
+        elif getattr(engine, "paired", None) and engine.paired[li]:  # two merges per tile
+            tiles = float(-(-len(lv.merges) // 2)) * g.units
         else:
             m = lv.merges
             tiles = float(sum(math.ceil((b - a) / tm) * math.ceil((c - b) / tn) for a, b, c in m.tolist()))

@@ -53,6 +53,13 @@ extern "C" {
  * row of exactly one tile) and writes knorm and fusable = (knorm > 0) itself -- replaces
  * the K pass of kvf_block_norms (core.py:115-119) with no extra HBM read. */
 #define KVF_SIM_WRITE_NORMS 0x100
+/* OR-ed into kvf_similarity_select's path (KVF_PATH_TC, direct rows): a level whose merges
+ * all have <= 128 blocks per side runs two merges per tile on the diagonal of the CTA
+ * pair's 256 x 256 product -- tile k = merges 2k (CTA 0) and 2k + 1 (CTA 1), tiles int32
+ * [ceil(nm / 2)][3] = {2k, 0, 0}; the tile's 16 partials slots are merge 2k's first 8 and
+ * merge 2k + 1's last 8 (kvf_level_stats tile offsets (m / 2) * 16 + (m % 2) * 8). Each CTA
+ * streams only its own merge's rows: half the operand bytes of one merge per tile. */
+#define KVF_SIM_PAIRED 0x200
 
 /* Library identity and last error (thread-local). */
 const char* kvf_last_error(void);

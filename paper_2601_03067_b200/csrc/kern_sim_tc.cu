@@ -206,6 +206,24 @@ __device__ __forceinline__ TileInfo rec_info(const int32_t* r, int nt, int64_t u
   return t;
 }
 
+// Paired small merges (every merge side of the level <= 128 blocks): a tile holds merge m on
+// CTA 0 and merge m + 1 on CTA 1, i.e. on the diagonal of the pair's 256 x 256 product --
+// CTA c streams its own merge's left blocks as A and its right blocks as its B half, and
+// only its own quadrant counts. The view shifts i0 / j0 so the shared address and index
+// arithmetic lands on merge m + c; `dead` marks the odd level's missing partner merge.
+__device__ __forceinline__ void pair_view(TileInfo& t, uint32_t crank, const int32_t* __restrict__ merges,
+                                          int nm, bool& dead) {
+  const int mc = t.m + (int)crank;
+  dead = mc >= nm;
+  const int mm = dead ? nm - 1 : mc;  // addresses of a real merge; its rows are masked
+  t.m = mm;
+  t.lb = t.pl = merges[3 * mm];
+  t.mid = t.pm = merges[3 * mm + 1];
+  t.re = t.pr = merges[3 * mm + 2];
+  t.i0 = -(int)crank * BM;
+  t.j0 = -(int)crank * BNH;
+}
+
 // 16-byte global -> shared copy on the LSU path (L2 only), completion tracked by an
 // mbarrier arrive-on (noinc: the barrier's expected count covers the arriving lanes)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
@@ -264,7 +282,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               int32_t* __restrict__ resc, int32_t* __restrict__ resc_count, int resc_cap,
               float resc_band, int32_t* __restrict__ work_counter, int gathered, int split3,
               int nsplit, float* __restrict__ spart, int32_t* __restrict__ scnt,
-              const __nv_bfloat16* __restrict__ pool, int fnorm) {
+              const __nv_bfloat16* __restrict__ pool, int fnorm, int nm, int paired) {
   // BMC = A rows per CTA: 128 (pair tile 256 x 256, two TMEM accumulators, the epilogue of
   // tile k overlaps the MMAs of tile k + 1) or 256 ("wide": pair tile 512 x 256, one
   // accumulator filling TMEM; per k-step a CTA loads 32 KB of A + 16 KB of B for twice the
@@ -305,7 +323,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
   uint64_t* norm_ready = mma_done + 8;                              // [2]
   float* anorm_b = reinterpret_cast<float*>(meta + 8192);
   float* bnorm_b = anorm_b + 2 * BM;
-  if (WIDE) fnorm = 0;
+  if (WIDE) fnorm = paired = 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = cta_rank();
@@ -376,7 +394,11 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
         break;
       }
-      const TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
+      TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
+      if (paired) {
+        bool dead;
+        pair_view(t, crank, merges, nm, dead);
+      }
       const int sk = sched_rec[sl * kRec + 10];
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
@@ -608,10 +630,13 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       mbar_wait_cluster(&sched_full[sl], (it / SCHED_DEPTH) & 1);
       const int w = sched_rec[sl * kRec];
       const int sk = sched_rec[sl * kRec + 10];
-      const TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
+      TileInfo t = rec_info(sched_rec + sl * kRec, nt, u0);
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&sched_empty[sl], 0);
       if (w < 0) break;
+      bool dead = false;
+      if (paired) pair_view(t, crank, merges, nm, dead);
+      const int cbeg = paired ? (int)crank * BNH : 0;  // first column of this CTA's merge
       const int mb = (int)(tc & 1);  // metadata buffer of this tile
       float* inv_j = inv_j_b + mb * BN;
       int32_t* colmin = colmin_b + mb * BN;
@@ -622,8 +647,8 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       const int64_t gb = t.u * g.NB;
       const int32_t* lv = live + gb;
       const int mi0 = t.i0 + (int)crank * BMC;
-      const int ni = max(0, min(BMC, t.pm - t.pl - mi0));  // valid rows of this CTA
-      const int nj = min(BN, t.pr - t.pm - t.j0);
+      const int ni = dead ? 0 : max(0, min(BMC, t.pm - t.pl - mi0));  // valid rows of this CTA
+      const int nj = dead ? cbeg : min(BN, t.pr - t.pm - t.j0);        // columns [cbeg, nj)
       if (fnorm) {
         // Key norms of the rows this CTA streams (level 1: every block is an operand row of
         // exactly one tile), read from the ring after the MMAs: thread et takes A row et
@@ -690,12 +715,13 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         mbar_wait_cluster(&norm_ready[mb], (tc >> 1) & 1);  // both CTAs' norms of this tile
       }
       for (int c = et; c < BN; c += ET) {  // column metadata
-        const int64_t bj = gb + (c < nj ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
+        const bool inc = c >= cbeg && c < nj;
+        const int64_t bj = gb + (inc ? (staged ? lv[t.pm + t.j0 + c] : t.mid + t.j0 + c) : 0);
         // independent loads (one round trip), combined afterwards
         const uint8_t al = alive[bj];
         const float nk = fnorm ? bnorm_b[mb * BN + c] : knorm[bj];
         const uint8_t fu = fnorm ? (nk > 0.f ? 1 : 0) : fusable[bj];
-        const bool ok = c < nj && al && fu;
+        const bool ok = inc && al && fu;
         colid[c] = (int32_t)(bj - gb);
         const float nv = ok ? nk : 0.f;
         ok_j[c] = ok;
@@ -825,7 +851,7 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
               mn = fminf(mn, sv);
               mx = fmaxf(mx, sv);
             }
-            if (row < ni && col < nj)
+            if (row < ni && col >= cbeg && col < nj)
               samp[(int64_t)(my_id - t.lb) * (t.re - t.mid) + (colid[col] - t.mid)] =
                   ok ? (double)sv : (double)NAN;
           }
@@ -1017,6 +1043,7 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   if (wide && (gathered || a.nsplit > 1)) return cudaErrorInvalidValue;
   if (a.write_norms && (wide || compact || a.nsplit > 1 || split3 || g.head_mode))
     return cudaErrorInvalidValue;
+  if (a.paired && (wide || compact)) return cudaErrorInvalidValue;
   auto kern = wide ? sim_tc_kernel<2 * BM> : sim_tc_kernel<BM>;
   const int smem_bytes = wide ? SMEM_BYTES_WIDE : SMEM_BYTES;
   static bool attr_set[2] = {false, false};
@@ -1057,7 +1084,8 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
       a.absorber, a.merges, a.tiles,
       a.nt, thr, a.partials, a.samples, a.sample_off, a.sample_stride, a.live, a.rank, a.resc,
       a.resc_count, (int)a.resc_cap, (float)a.resc_band, counter, gathered ? gmode : 0, split3 ? 1 : 0,
-      nsplit, a.split_part, a.split_count, (const __nv_bfloat16*)a.pool, a.write_norms && !wide ? 1 : 0);
+      nsplit, a.split_part, a.split_count, (const __nv_bfloat16*)a.pool, a.write_norms && !wide ? 1 : 0,
+      a.nm, a.paired);
   return cudaGetLastError();
 }
 

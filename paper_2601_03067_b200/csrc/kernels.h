@@ -56,6 +56,8 @@ struct SimArgs {
   // level 1 only: the launch computes the key norm of every streamed row (knorm written,
   // fusable = knorm > 0) instead of reading them (KVF_SIM_WRITE_NORMS)
   int write_norms = 0;
+  // paired small merges (KVF_SIM_PAIRED): tile k holds merges 2k (CTA 0) and 2k + 1 (CTA 1)
+  int paired = 0;
 };
 
 struct RescoreArgs {

@@ -162,8 +162,14 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
   a.split_count = split_count;
   if (filter && dtype != F32)
     return fail(KVF_ERR_INVALID, "a bf16 operand copy (filter) is for float32 pools");
-  if (path & KVF_SIM_WRITE_NORMS) {
-    path &= ~KVF_SIM_WRITE_NORMS;
+  const int sim_flags = path & (KVF_SIM_PAIRED | KVF_SIM_WRITE_NORMS);
+  path &= ~(KVF_SIM_PAIRED | KVF_SIM_WRITE_NORMS);
+  if (sim_flags & KVF_SIM_PAIRED) {
+    if (path != KVF_PATH_TC || live)
+      return fail(KVF_ERR_INVALID, "KVF_SIM_PAIRED needs the narrow tcgen05 tile and direct rows");
+    a.paired = 1;
+  }
+  if (sim_flags & KVF_SIM_WRITE_NORMS) {
     if (path != KVF_PATH_TC || dtype != BF16 || head_mode || nsplit != 1 || live || filter)
       return fail(KVF_ERR_INVALID,
                   "KVF_SIM_WRITE_NORMS needs the narrow tcgen05 tile, a bf16 pool, folded units, "

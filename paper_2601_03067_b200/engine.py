@@ -114,6 +114,22 @@ class _PlanDevice:
             )
 
 
+def _paired_level(base: dict, ppt: int, device) -> dict:
+    """Device arrays of a level run as paired small merges (KVF_SIM_PAIRED): tile k =
+    merges 2k and 2k + 1 on the diagonal of one pair tile; merge m owns partial slots
+    [(m // 2) * ppt + (m % 2) * ppt / 2, + ppt / 2)."""
+    nm = base["nm"]
+    nt = (nm + 1) // 2
+    tiles = np.zeros((nt, 3), dtype=np.int32)
+    tiles[:, 0] = np.arange(0, nm, 2, dtype=np.int32)
+    m = np.arange(nm + 1)
+    off_p = ((m // 2) * ppt + (m % 2) * (ppt // 2)).astype(np.int32)
+    d = dict(base)
+    d.update(tiles=torch.from_numpy(tiles).to(device), tile_off=None,
+             tile_off_p=torch.from_numpy(off_p).to(device), nt=nt, paired=True)
+    return d
+
+
 def _plan_device(plan: Plan, tm: int, tn: int, ppt: int, device) -> _PlanDevice:
     cache = plan.__dict__.setdefault("_device_cache", {})
     key = (tm, tn, ppt, str(device))
@@ -240,6 +256,19 @@ class FusionEngine:
         # hi / lo bf16 split of a float32 pool (kvf_convert_rows), 2 x the pool's elements
         self.filter = (torch.empty(2 * geom.L * NB * geom.E, dtype=torch.bfloat16, device=dev)
                        if self.filter_mode else None)
+        # paired small merges (KVF_SIM_PAIRED): a level whose merge sides all fit one
+        # 128-row box runs two merges per tile on the pair tile's diagonal, each CTA streaming
+        # only its own merge's rows (cfg3 level 1: 128 x 128 merges; cfg1: 64 / 128)
+        self.levels = list(self.pdev.levels)
+        self.paired = [False] * len(self.levels)
+        if path == N.PATH_TC and os.environ.get("KVF_SIM_PAIRED", "1") != "0":
+            for li, lvp in enumerate(plan.levels):
+                compacted = compact_from is not None and lvp.height >= compact_from
+                m_ = lvp.merges
+                if (len(m_) >= 2 and not compacted and int((m_[:, 1] - m_[:, 0]).max()) <= self.tm // 2
+                        and int((m_[:, 2] - m_[:, 1]).max()) <= self.tn // 2):
+                    self.paired[li] = True
+                    self.levels[li] = _paired_level(self.levels[li], self.ppt, self.device)
         # split-K per level (tcgen05 path): few, long-K tiles (cfg1, CFF) spread over all SMs
         self.nsplit = [1] * len(self.pdev.levels)
         self.split_part = self.split_count = None
@@ -249,7 +278,7 @@ class FusionEngine:
         if path == N.PATH_TC and split:
             nk = geom.r // 64 * (3 if self.filter_mode else 1)
             need, tiles_max = 0, 0
-            for li, lv in enumerate(self.pdev.levels):
+            for li, lv in enumerate(self.levels):
                 compacted = compact_from is not None and plan.levels[li].height >= compact_from
                 if compacted and compact_mode == "gathered":
                     continue
@@ -268,13 +297,12 @@ class FusionEngine:
         # narrow tile's 128 FLOP per L2->SM byte leaves the tensor pipe ~20% idle on the
         # crossbar; the wide tile gives up the double-buffered TMEM accumulator for 171
         self.wide = [False] * len(self.pdev.levels)
-        self.levels = list(self.pdev.levels)
         if path == N.PATH_TC and geom.head_mode == 0 and compact_mode != "gathered":
             wide_env = os.environ.get("KVF_SIM_WIDE", "auto")
             tmw, _, _ = tile_shape(dtype, 0, N.PATH_TC_WIDE)
             pdw = None
             for li, lvp in enumerate(plan.levels):
-                if self.nsplit[li] != 1 or wide_env == "0" or not len(lvp.merges):
+                if self.nsplit[li] != 1 or wide_env == "0" or not len(lvp.merges) or self.paired[li]:
                     continue
                 left_min = int((lvp.merges[:, 1] - lvp.merges[:, 0]).min())
                 if pdw is None:
@@ -452,7 +480,8 @@ class FusionEngine:
                     self.nsplit[li], N.ptr(self.split_part) if self.nsplit[li] > 1 else None,
                     N.ptr(self.split_count) if self.nsplit[li] > 1 else None,
                     (N.PATH_TC_WIDE if self.wide[li] else self.path)
-                    | (N.SIM_WRITE_NORMS if fuse_knorm and li == 0 else 0), sp,
+                    | (N.SIM_WRITE_NORMS if fuse_knorm and li == 0 else 0)
+                    | (N.SIM_PAIRED if self.paired[li] else 0), sp,
                 )
                 if self.rescore_cap:
                     launches += 1

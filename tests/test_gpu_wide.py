@@ -18,6 +18,7 @@ from paper_2601_03067_b200.workload import synthetic_kv  # noqa: E402
 
 def _engine(monkeypatch, wide, geom, plan, dtype, device, **kw):
     monkeypatch.setenv("KVF_SIM_WIDE", "1" if wide else "0")
+    monkeypatch.setenv("KVF_SIM_PAIRED", "0")  # every level on the tile under test
     return FusionEngine(geom, plan, dtype, device, split=False, **kw)
 
 
