@@ -95,3 +95,31 @@ def test_schedule_and_compaction_argument_errors():
     assert rc == N.KVF_ERR_INVALID
     assert lib.kvf_remap_ids(None, -1, None, 0, None, None) == N.KVF_ERR_INVALID
     assert lib.kvf_remap_ids(None, 0, None, 0, None, None) == N.KVF_OK  # empty: nothing to do
+
+
+def test_similarity_path_flags_validate_before_cuda():
+    """Wide tile / paired merges / fused level-1 norms: unsupported combinations are refused
+    before any CUDA call (nt = 0, so no device pointer is touched)."""
+    lib = N.lib()
+    x = C.c_int()
+    p = C.addressof(x)
+
+    def sel(dtype, head_mode, nsplit, path, live=None, staged=None, filt=None):
+        return lib.kvf_similarity_select(None, dtype, 1, 256, 16, 8, 128, head_mode, 0, 1, None, None,
+                                         None, None, None, 0, None, 0, 0.8, None, None, None, 0,
+                                         live, live, staged, None, 0, 0.0, filt, None, None, nsplit,
+                                         p if nsplit > 1 else None, p if nsplit > 1 else None, path, None)
+
+    rc = sel(2, 0, 2, N.PATH_TC_WIDE)
+    assert rc == N.KVF_ERR_INVALID and "nsplit" in lib.kvf_last_error().decode()
+    rc = sel(2, 0, 1, N.PATH_TC_WIDE, live=p)  # gathered compaction (no staged rows)
+    assert rc == N.KVF_ERR_INVALID and "staged" in lib.kvf_last_error().decode()
+    rc = sel(2, 0, 1, N.PATH_TC | N.SIM_PAIRED, live=p, staged=p)
+    assert rc == N.KVF_ERR_INVALID and "KVF_SIM_PAIRED" in lib.kvf_last_error().decode()
+    rc = sel(2, 0, 1, N.PATH_TC_WIDE | N.SIM_PAIRED)
+    assert rc == N.KVF_ERR_INVALID and "KVF_SIM_PAIRED" in lib.kvf_last_error().decode()
+    for args in ((1, 0, 1), (2, 1, 1), (2, 0, 2)):  # float32 pool, per-head units, split-K
+        rc = sel(*args, N.PATH_TC | N.SIM_WRITE_NORMS, filt=p if args[0] == 1 else None)
+        assert rc == N.KVF_ERR_INVALID and "KVF_SIM_WRITE_NORMS" in lib.kvf_last_error().decode()
+    rc = sel(2, 0, 1, N.PATH_TC_WIDE | N.SIM_WRITE_NORMS)
+    assert rc == N.KVF_ERR_INVALID and "KVF_SIM_WRITE_NORMS" in lib.kvf_last_error().decode()
