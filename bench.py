@@ -726,6 +726,31 @@ def ours_main(args):
         dist.destroy_process_group()
 
 
+def measure_tf32_tflops(torch, dev, n: int = 8192) -> float | None:
+    """TF32 tensor-core throughput of this box (not in MEASURED_PEAKS.json):
+    cuBLAS float32 matmul with TF32 allowed, best of 5 after warm-up."""
+    try:
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(n, n, device=dev)
+        b = torch.randn(n, n, device=dev)
+        for _ in range(3):
+            a @ b
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            a @ b
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        torch.backends.cuda.matmul.allow_tf32 = prev
+        del a, b
+        return 2.0 * n ** 3 / (best / 1e3) / 1e12
+    except Exception:
+        return None
+
+
 def sim_work(st, engine) -> dict:
     """Similarity work of one fusion run from its MergeRecord counters (level_stats[..., 0:2] =
     alive fusable left / right blocks per merge):
@@ -923,11 +948,19 @@ def bench_subconfig(name, dev, torch, steps=10, warmup=3, skip_cpu=False):
         res["roofline"]["tensor"]["fp32_cuda_core_peak"] = 148 * 128 * 2 * mhz * 1e6 / 1e12
         res["roofline"]["tensor"]["frac_of_fp32_cuda_core_peak"] = (
             achieved / res["roofline"]["tensor"]["fp32_cuda_core_peak"])
-        res["roofline"]["note"] = ("4 layers x 512 blocks: 3 levels of 16 / 8 / 4 tiles (split-K over all SMs); "
-                                   "each launch is a few microseconds of work, so launch latency bounds it")
+        tf32 = measure_tf32_tflops(torch, dev)
+        if tf32:
+            res["roofline"]["tensor"]["tf32_tflops_measured"] = tf32
+            res["roofline"]["tensor"]["frac_of_tf32_measured"] = achieved / tf32
+            res["roofline"]["tensor"]["tf32_how"] = ("torch.matmul float32 8192^3 with allow_tf32 (cuBLAS "
+                                                     "TF32 tensor cores), best of 5, this box")
+        res["roofline"]["note"] = ("4 layers x 512 blocks: 3 levels of 8 / 4 / 4 tiles (levels 1-2 pair two "
+                                   "merges per tile; split-K over all SMs); each launch is a few microseconds "
+                                   "of work, so launch latency bounds it")
     if c["variant"] == "cff":
-        res["roofline"]["note"] = ("CFF level-1 merges are 128 x 128 blocks inside 256 x 256 tiles; the step "
-                                   "moves 2.1 GB of K+V for norms and ~3 GB of operand rows for similarity")
+        res["roofline"]["note"] = ("CFF level-1 merges are 128 x 128 blocks, two per 256 x 256 tile on its "
+                                   "diagonal (each CTA streams its own merge's rows); the level-1 launch also "
+                                   "computes the key norms; the V norms read 1.1 GB")
     layers = list(range(min(L, ref_concurrency(name, cap=8))))
     par = gpu_parity_state(st, plan, layers)
     res["parity"] = {"exact_mode": bool(st.exact), "inexact_pairs_per_step": st.inexact_pairs()}
