@@ -29,6 +29,16 @@ for dt in (torch.bfloat16, torch.float32):
     torch.cuda.synchronize()
     print("wide + chunked stats", dt, outs[0].report.compression_ratio)
 del os.environ["KVF_SIM_WIDE"], os.environ["KVF_LS_CHUNKED"]
+# paired level-1 merges with the key norms fused into the launch (no split-K)
+from paper_2601_03067_b200.engine import FusionEngine, Geometry  # noqa: E402
+from paper_2601_03067_b200.schedule import bff_plan  # noqa: E402
+Kt, Vt = synthetic_kv(2, 16, 64, 16, 8, 128, dtype=torch.bfloat16, seed=12)
+eng = FusionEngine(Geometry(2, 16 * 64, 16, 8, 128, 0), bff_plan(16, 64, None), torch.bfloat16, Kt.device,
+                   split=False)
+assert eng.paired[0] and eng.fuse_knorm
+st = eng.run(Kt.reshape(-1).clone(), Vt.reshape(-1).clone(), 0.8, keep_samples=True)
+torch.cuda.synchronize()
+print("paired + fused norms", int(st.live_count.sum()))
 # compacted levels with the alive rows gathered from the pool (cp.async + peer relay)
 from paper_2601_03067_b200 import _native as N  # noqa: E402
 from paper_2601_03067_b200.engine import FusionEngine, Geometry  # noqa: E402
