@@ -174,7 +174,10 @@ int kvf_level_stats(int64_t u0, int64_t nU, int64_t U, int64_t NB,
  * key absorber's new unit direction is written to its row (taken from
  * *shadow_count on its first fusion, up to shadow_cap; overflowing absorbers
  * keep sidx = -1 and the count exceeds the cap); the pool still receives
- * bf16(s_home * dir). r <= 16384. */
+ * bf16(s_home * dir). r <= 16384. which | KVF_MERGE_LAST_LEVEL: the tree's last
+ * level -- shadow rows are still read but no longer written (nothing reads them
+ * after the last merge). */
+#define KVF_MERGE_LAST_LEVEL 0x10
 int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L,
                      int64_t NB, int t, int h, int d, int head_mode, void* knorm,
                      void* vnorm, const void* orig_knorm, const void* orig_vnorm,

@@ -29,6 +29,7 @@ PATH_TC = 2
 PATH_TC_WIDE = 3  # tcgen05, 512 x 256 tile per CTA pair
 SIM_WRITE_NORMS = 0x100  # OR-ed into the path: level-1 launch computes the key norms
 SIM_PAIRED = 0x200  # OR-ed into the path: two small merges per tile (diagonal)
+MERGE_LAST_LEVEL = 0x10  # OR-ed into kvf_merge_groups' which: shadow rows read, not written
 
 DT_F64, DT_F32, DT_BF16 = 0, 1, 2
 

@@ -484,6 +484,7 @@ struct ExactArgs {
   int64_t cap;
   int32_t* sidx;     // [U][NB]
   int32_t* scount;   // rows taken (can exceed cap: overflow is reported)
+  int write_rows = 1;  // 0 at the tree's last level: rows are read, never written again
 };
 
 template <typename T, int EPT>
@@ -746,7 +747,7 @@ merge_tma_kernel(T* __restrict__ pool_k, T* __restrict__ pool_v, Geom g, float* 
     // exact mode, keys: the absorber's shadow row (taken on its first fusion); published
     // through the norm reduction's barriers (every consumer reads it before the next
     // item's reduction, the only place it is written again)
-    const bool want_row = ex.shadow && !is_v;
+    const bool want_row = ex.shadow && !is_v && ex.write_rows;
     if (want_row && ct == 0) {
       int sl = mt.ash;
       if (sl < 0) {
@@ -1178,7 +1179,7 @@ merge_ring_kernel(__nv_bfloat16* __restrict__ pool_k, __nv_bfloat16* __restrict_
     // exact mode, keys: the absorber's shadow row (taken on its first fusion)
     float* srow = nullptr;
     const float inv_n = nrm > 0.f ? 1.f / nrm : 0.f;
-    if (ex.shadow && !is_v) {
+    if (ex.shadow && !is_v && ex.write_rows) {
       int sl = m.ash;
       if (sl < 0) {
         if (lane == 0) {
@@ -1374,7 +1375,7 @@ cudaError_t merge_dispatch(void* pk, void* pv, const Geom& g, void* kn, void* vn
         if (e != cudaSuccess || sel.which == 1) return e;
       }
       sel = ItemSel{2};
-      ex = ExactArgs{nullptr, 0, nullptr, nullptr};
+      ex = ExactArgs{nullptr, 0, nullptr, nullptr, 0};
     }
   }
   if constexpr (std::is_same<T, __nv_bfloat16>::value) {
@@ -1444,9 +1445,11 @@ cudaError_t launch_merge_groups(void* pool_k, void* pool_v, int dtype, const Geo
                                 void* knorm, void* vnorm, const void* oknorm,
                                 const void* ovnorm, int32_t* level_ws, int which, float* shadow,
                                 int64_t shadow_cap, int32_t* sidx, int32_t* scount, cudaStream_t s) {
+  const int write_rows = (which & kMergeLastLevel) ? 0 : 1;
+  which &= ~kMergeLastLevel;
   if (which < 1 || which > 3) return cudaErrorInvalidValue;
   const ItemSel sel{which};
-  const ExactArgs ex{shadow, shadow_cap, sidx, scount};
+  const ExactArgs ex{shadow, shadow_cap, sidx, scount, write_rows};
   if (shadow && dtype != BF16) return cudaErrorInvalidValue;
   const int64_t n_total = g.units() * g.NB;
   switch (dtype) {

@@ -84,6 +84,7 @@ cudaError_t launch_sim_simt(const SimArgs& a, cudaStream_t s);
 
 // tcgen05 path (bf16 only): one 256 x 256 tile per CTA pair (cta_group::2),
 // similarity partials written per CTA (2 slots per tile)
+constexpr int kMergeLastLevel = 0x10;  // = KVF_MERGE_LAST_LEVEL (include/kvfuse_b200.h)
 constexpr int kTcTileM = 256;
 constexpr int kTcTileMWide = 512;
 constexpr int kTcTileN = 256;

@@ -246,7 +246,9 @@ int kvf_merge_groups(void* pool_k, void* pool_v, int dtype, int64_t L, int64_t N
   if (shadow && g.r() > 16384)
     return fail(KVF_ERR_INVALID, "exact mode supports block vectors up to 16384 elements, got %lld",
                 (long long)g.r());
-  if (which < 1 || which > 3) return fail(KVF_ERR_INVALID, "which must be 1 (K), 2 (V) or 3 (K and V)");
+  const int which_sel = which & ~KVF_MERGE_LAST_LEVEL;
+  if (which_sel < 1 || which_sel > 3)
+    return fail(KVF_ERR_INVALID, "which must be 1 (K), 2 (V) or 3 (K and V)");
   if (shadow) {
     if (dtype != BF16) return fail(KVF_ERR_INVALID, "exact mode (shadow rows) is for bfloat16 pools");
     if (!sidx || !shadow_count) return fail(KVF_ERR_INVALID, "shadow rows need sidx and shadow_count");

@@ -501,7 +501,8 @@ class FusionEngine:
             )
             N.call(
                 "kvf_merge_groups", N.ptr(pool_k), N.ptr(pool_v), dt, *g.args(), N.ptr(knorm),
-                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws), 3,
+                N.ptr(vnorm), N.ptr(oknorm), N.ptr(ovnorm), N.ptr(self.level_ws),
+                3 | (N.MERGE_LAST_LEVEL if li == len(self.levels) - 1 else 0),
                 N.ptr(self.shadow), self.shadow_cap, N.ptr(self.sidx), N.ptr(self.scount), sp,
             )
             if self.filter is not None:  # refresh the bf16 copy of the rewritten keys

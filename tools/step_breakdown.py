@@ -110,7 +110,8 @@ for li, lv in enumerate(plan.levels):
     if eng.exact:
         sh_mem = int((member & seen_abs).sum())
         sh_abs = int((absr & seen_abs).sum())
-        extra = (sh_mem + sh_abs) * vb + n_abs * 2 * vb  # fp32 reads (2x) + fp32 row writes
+        last = li == len(plan.levels) - 1  # the last level writes no shadow rows
+        extra = (sh_mem + sh_abs) * vb + (0 if last else n_abs * 2 * vb)  # fp32 reads (2x) + row writes
     seen_abs |= absr
     gb = (base + extra) / 1e9
     ms = merge_ms[li] if li < len(merge_ms) else float("nan")
