@@ -24,7 +24,7 @@ def _run(monkeypatch, paired, geom, plan, Kt, Vt, dtype, samples, **kw):
     return st, eng
 
 
-@pytest.mark.parametrize("case", ["cff", "bff_odd", "bff_f32_split", "bff_norms"])
+@pytest.mark.parametrize("case", ["cff", "bff_odd", "bff_f32_split", "bff_norms", "per_head", "group_size"])
 @pytest.mark.parametrize("samples", [False, True], ids=["moments", "samples"])
 def test_paired_matches_single(monkeypatch, case, samples):
     t, h, d = 16, 8, 128
@@ -42,12 +42,20 @@ def test_paired_matches_single(monkeypatch, case, samples):
         L, B, p = 4, 8, 64
         Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=63)
         plan = bff_plan(B, p, None)
+    elif case == "per_head":  # (layer, KV head) units: head-slice rows on paired tiles
+        L, B, p = 2, 8, 64
+        Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=65)
+        plan = bff_plan(B, p, None)
+    elif case == "group_size":  # independent trees of 3 rows (uneven merges inside a level)
+        L, B, p = 2, 12, 96
+        Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=66)
+        plan = bff_plan(B, p, 3)
     else:  # fused level-1 key norms on paired tiles
         L, B, p = 8, 32, 128
         Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=dtype, seed=64)
         plan = bff_plan(B, p, None)
         kw = dict(split=False)
-    geom = K.Geometry(L, B * p, t, h, d, 0)
+    geom = K.Geometry(L, B * p, t, h, d, 1 if case == "per_head" else 0)
     a, ea = _run(monkeypatch, True, geom, plan, Kt, Vt, dtype, samples, **kw)
     b, eb = _run(monkeypatch, False, geom, plan, Kt, Vt, dtype, samples, **kw)
     split_any = max(ea.nsplit) > 1 or max(eb.nsplit) > 1
