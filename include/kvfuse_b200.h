@@ -47,8 +47,8 @@ extern "C" {
 #define KVF_PATH_TC 2    /* tcgen05 + TMEM + TMA similarity (bf16 pools only) */
 #define KVF_PATH_TC_WIDE 3 /* tcgen05, 512 x 256 tile per CTA pair (one TMEM
                               accumulator; nsplit == 1, staged or direct rows) */
-/* OR-ed into kvf_similarity_select's path (KVF_PATH_TC, bf16 pool, folded units,
- * nsplit == 1, direct rows): the launch computes the key norm of every row it streams
+/* OR-ed into kvf_similarity_select's path (KVF_PATH_TC, bf16 pool, nsplit == 1, direct
+ * rows; folded or per-head units): the launch computes the key norm of every row it streams
  * from the shared-memory stages (the tree's first level, where each block is an operand
  * row of exactly one tile) and writes knorm and fusable = (knorm > 0) itself -- replaces
  * the K pass of kvf_block_norms (core.py:115-119) with no extra HBM read. */

@@ -1041,7 +1041,7 @@ cudaError_t launch_sim_tc(const SimArgs& a, cudaStream_t s) {
   if (res != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const bool wide = a.wide != 0;
   if (wide && (gathered || a.nsplit > 1)) return cudaErrorInvalidValue;
-  if (a.write_norms && (wide || compact || a.nsplit > 1 || split3 || g.head_mode))
+  if (a.write_norms && (wide || compact || a.nsplit > 1 || split3))
     return cudaErrorInvalidValue;
   if (a.paired && (wide || compact)) return cudaErrorInvalidValue;
   auto kern = wide ? sim_tc_kernel<2 * BM> : sim_tc_kernel<BM>;

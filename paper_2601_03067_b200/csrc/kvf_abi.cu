@@ -170,10 +170,10 @@ int kvf_similarity_select(const void* pool_k, int dtype, int64_t L, int64_t NB, 
     a.paired = 1;
   }
   if (sim_flags & KVF_SIM_WRITE_NORMS) {
-    if (path != KVF_PATH_TC || dtype != BF16 || head_mode || nsplit != 1 || live || filter)
+    if (path != KVF_PATH_TC || dtype != BF16 || nsplit != 1 || live || filter)
       return fail(KVF_ERR_INVALID,
-                  "KVF_SIM_WRITE_NORMS needs the narrow tcgen05 tile, a bf16 pool, folded units, "
-                  "nsplit == 1 and direct rows");
+                  "KVF_SIM_WRITE_NORMS needs the narrow tcgen05 tile, a bf16 pool, nsplit == 1 "
+                  "and direct rows");
     a.write_norms = 1;
   }
   if (path == KVF_PATH_AUTO) path = (dtype == BF16 || filter) ? KVF_PATH_TC : KVF_PATH_SIMT;

@@ -317,7 +317,7 @@ class FusionEngine:
         # in a level-1 merge whose sides fit one narrow tile; saves the K pass of the norms
         # (17 GB read per cfg2 step)
         self.fuse_knorm = False
-        if (path == N.PATH_TC and dtype == torch.bfloat16 and geom.head_mode == 0 and plan.levels
+        if (path == N.PATH_TC and dtype == torch.bfloat16 and plan.levels
                 and os.environ.get("KVF_FUSE_KNORM", "1") != "0"):
             lv0 = plan.levels[0]
             m0 = lv0.merges

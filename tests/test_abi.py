@@ -118,7 +118,7 @@ def test_similarity_path_flags_validate_before_cuda():
     assert rc == N.KVF_ERR_INVALID and "KVF_SIM_PAIRED" in lib.kvf_last_error().decode()
     rc = sel(2, 0, 1, N.PATH_TC_WIDE | N.SIM_PAIRED)
     assert rc == N.KVF_ERR_INVALID and "KVF_SIM_PAIRED" in lib.kvf_last_error().decode()
-    for args in ((1, 0, 1), (2, 1, 1), (2, 0, 2)):  # float32 pool, per-head units, split-K
+    for args in ((1, 0, 1), (2, 0, 2)):  # float32 pool, split-K
         rc = sel(*args, N.PATH_TC | N.SIM_WRITE_NORMS, filt=p if args[0] == 1 else None)
         assert rc == N.KVF_ERR_INVALID and "KVF_SIM_WRITE_NORMS" in lib.kvf_last_error().decode()
     rc = sel(2, 0, 1, N.PATH_TC_WIDE | N.SIM_WRITE_NORMS)

@@ -24,7 +24,7 @@ def _run(monkeypatch, fused, geom, plan, Kt, Vt, **kw):
     return st
 
 
-@pytest.mark.parametrize("case", ["bff", "bff_ragged", "cff", "zero_blocks"])
+@pytest.mark.parametrize("case", ["bff", "bff_ragged", "cff", "zero_blocks", "per_head"])
 def test_fused_knorm_matches_separate_pass(monkeypatch, case):
     t, h, d = 16, 8, 128
     if case == "cff":
@@ -38,7 +38,7 @@ def test_fused_knorm_matches_separate_pass(monkeypatch, case):
     if case == "zero_blocks":  # not fusable: key norm 0 (fusion.py:218)
         Kt[:, 3, 7] = 0
         Kt[:, 11, 0] = 0
-    geom = K.Geometry(L, B * p, t, h, d, 0)
+    geom = K.Geometry(L, B * p, t, h, d, 1 if case == "per_head" else 0)
     a = _run(monkeypatch, True, geom, plan, Kt, Vt)
     b = _run(monkeypatch, False, geom, plan, Kt, Vt)
     rel = ((a.orig_knorm - b.orig_knorm).abs() / b.orig_knorm.clamp(min=1e-30)).max().item()
@@ -46,6 +46,7 @@ def test_fused_knorm_matches_separate_pass(monkeypatch, case):
     assert torch.equal(a.fusable, b.fusable)
     if case == "zero_blocks":
         assert int((a.fusable == 0).sum()) == 2 * L
+    assert torch.equal(a.orig_knorm, b.orig_knorm)  # same partials, exact float64 sums
     assert torch.equal(a.absorber, b.absorber)
     assert torch.equal(a.table, b.table) and torch.equal(a.refcount, b.refcount)
     assert torch.equal(a.pool_k.view(torch.int16), b.pool_k.view(torch.int16))
@@ -62,10 +63,8 @@ def test_fused_knorm_selection(monkeypatch):
     dev = torch.device("cuda", 0)
     g = K.Geometry(4, 64 * 256, 16, 8, 128, 0)
     assert FusionEngine(g, bff_plan(64, 256, None), torch.bfloat16, dev).fuse_knorm  # cfg2 shape
-    # a row outside every level-1 merge (odd batch), per-head units, float32 pools: separate pass
+    # a row outside every level-1 merge (odd batch), float32 pools: separate pass
     assert not FusionEngine(K.Geometry(1, 5 * 64, 16, 8, 128, 0), bff_plan(5, 64, None),
-                            torch.bfloat16, dev).fuse_knorm
-    assert not FusionEngine(K.Geometry(1, 16 * 64, 16, 8, 128, 1), bff_plan(16, 64, None),
                             torch.bfloat16, dev).fuse_knorm
     assert not FusionEngine(K.Geometry(1, 16 * 64, 16, 8, 128, 0), bff_plan(16, 64, None),
                             torch.float32, dev).fuse_knorm
