@@ -739,8 +739,10 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
       int cnt = 0;
       double* samp = samples ? samples + t.ul * sample_stride + sample_off[t.m] : nullptr;
       asm volatile("bar.sync 1, %0;" ::"n"(ET) : "memory");  // column metadata visible
-      flush(mb ^ 1);  // the previous tile's first matches (every warp is past it)
-      prev_gb = gb;
+      if (nsplit > 1) {  // the previous tile's first matches (every warp is past it)
+        flush(mb ^ 1);
+        prev_gb = gb;
+      }
 
       const uint32_t acc = tc % NACC;
       mbar_wait(&tmem_full[acc], (tc / NACC) & 1);
@@ -896,6 +898,11 @@ sim_tc_kernel(const __grid_constant__ CUtensorMap tmap, Geom g, int64_t u0, int6
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(&tmem_empty[acc], 0);
+        // the previous tile's first matches, flushed only now: the cluster-scope release
+        // of the arrive above waits for this thread's outstanding global atomics, so the
+        // flush no longer delays the MMA warp's next accumulator (short per-head tiles)
+        flush(mb ^ 1);
+        prev_gb = gb;
       }
       ++tc;
       // this warp's similarity moments -> its own slot (fp32 warp tree, fixed order)

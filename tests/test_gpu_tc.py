@@ -95,7 +95,7 @@ def test_tc_compaction_bitwise(shape, head_mode, compact_from, mode):
     for sa, sb in zip(a.level_stats, b.level_stats):
         # counts / min / max exact; sums regroup across tiles -> fp rounding
         assert torch.equal(sa[..., [0, 1, 2, 3, 6, 7]], sb[..., [0, 1, 2, 3, 6, 7]])
-        torch.testing.assert_close(sa[..., 4:6], sb[..., 4:6], rtol=1e-7, atol=1e-9)
+        torch.testing.assert_close(sa[..., 4:6], sb[..., 4:6], rtol=1e-6, atol=1e-9)
     for xa, xb in zip(a.level_samples, b.level_samples):
         assert torch.equal(xa.isnan(), xb.isnan())
         assert torch.equal(torch.nan_to_num(xa), torch.nan_to_num(xb))
