@@ -192,6 +192,19 @@ def test_large_groups_vs_oracle(dtype, head_mode):
 def test_random_shapes_vs_oracle(seed):
     """Seeded random geometries (batch, blocks per request, heads, head dim, threshold,
     dtype, head mode, group size) against the float64 oracle."""
+    _random_case(seed)
+
+
+@pytest.mark.parametrize("seed", range(8, 8 + int(__import__("os").environ.get("KVF_RANDOM_CASES", "8"))))
+def test_random_shapes_forced_variants_vs_oracle(seed, monkeypatch):
+    """The same sweep with every level on the wide tile where split-K allows it and the
+    chunked level statistics on every level (paired merges and fused key norms as auto)."""
+    monkeypatch.setenv("KVF_SIM_WIDE", "1")
+    monkeypatch.setenv("KVF_LS_CHUNKED", "1")
+    _random_case(seed)
+
+
+def _random_case(seed):
     rng = np.random.default_rng(1000 + seed)
     B = int(rng.integers(2, 17))
     p = int(rng.choice([3, 8, 13, 32, 96]))  # 96: merges span several 256-block tiles
