@@ -197,6 +197,98 @@ class FusionState:
         return max(0, int(self.shadow_count.item()) - self.shadow_cap)
 
 
+@dataclass
+class TilePlan:
+    """Per-level similarity launch choices of a FusionEngine (host-only, no device state)."""
+
+    compact_from: int | None
+    paired: list  # two small merges per tile on the pair tile's diagonal (KVF_SIM_PAIRED)
+    nsplit: list  # split-K factor
+    wide: list  # 512 x 256 tile per CTA pair (KVF_PATH_TC_WIDE)
+    nt: list  # tiles per unit of the chosen tiling
+    fuse_knorm: bool  # level-1 launch writes the key norms (KVF_SIM_WRITE_NORMS)
+
+
+def auto_compact_from(plan: Plan) -> int | None:
+    """Lowest compacted tree height: depth - 1 (dead blocks are ~55% of the top merges'
+    rectangles); one lower when those merges span >= COMPACT_BIG_MERGE blocks (their
+    rectangle cost grows with the merge size while staging grows with the block count:
+    cfg5 shape, heights 6-8 compacted 571 -> 534-547 ms per layer; heights 5-8: 551 ms)."""
+    compact_from = plan.tree_depth - 1 if plan.tree_depth >= 4 else None
+    if compact_from is not None and compact_from - 1 >= 2:
+        lo = [lv for lv in plan.levels if lv.height == compact_from - 1]
+        if lo and len(lo[0].merges) and int((lo[0].merges[:, 2] - lo[0].merges[:, 0]).min()) >= COMPACT_BIG_MERGE:
+            compact_from -= 1
+    return compact_from
+
+
+def tile_plan(plan: Plan, geom: Geometry, dtype: torch.dtype, path: int, compact_from, compact_mode: str,
+              split: bool, pairs: int, env=None) -> TilePlan:
+    """Choose, per tree level, the similarity launch: paired small merges, split-K, the wide
+    tile, and whether level 1 computes the key norms. Pure host logic over the plan
+    (`env` defaults to os.environ: the KVF_SIM_* A/B knobs)."""
+    env = os.environ if env is None else env
+    U = geom.units
+    filter_mode = path == N.PATH_TC and dtype == torch.float32
+    if compact_from == "auto":
+        compact_from = auto_compact_from(plan)
+    if path != N.PATH_TC or geom.d % 8 != 0 or filter_mode:
+        compact_from = None
+    nlv = len(plan.levels)
+    tp = TilePlan(compact_from, [False] * nlv, [1] * nlv, [False] * nlv, [0] * nlv, False)
+    if path != N.PATH_TC:
+        tm = tn = _simt_tile()
+        for li, lv in enumerate(plan.levels):
+            tp.nt[li] = int(lv.tiling(tm, tn)[0].shape[0])
+        return tp
+    tm, tn, _ = tile_shape(dtype, geom.head_mode, path)
+    compacted = [compact_from is not None and lv.height >= compact_from for lv in plan.levels]
+    for li, lv in enumerate(plan.levels):
+        tp.nt[li] = int(lv.tiling(tm, tn)[0].shape[0])
+        m_ = lv.merges
+        # paired small merges: every merge side fits one 128-row box
+        if (env.get("KVF_SIM_PAIRED", "1") != "0" and len(m_) >= 2 and not compacted[li]
+                and int((m_[:, 1] - m_[:, 0]).max()) <= tm // 2 and int((m_[:, 2] - m_[:, 1]).max()) <= tn // 2):
+            tp.paired[li] = True
+            tp.nt[li] = (len(m_) + 1) // 2
+    # split-K: few, long-K tiles (cfg1, CFF) spread over all SMs
+    if split:
+        nk = geom.r // 64 * (3 if filter_mode else 1)
+        for li in range(nlv):
+            if compacted[li] and compact_mode == "gathered":
+                continue
+            n_tiles = tp.nt[li] * U
+            s_ = choose_split(n_tiles, nk, pairs)
+            while s_ > 1 and n_tiles * s_ * _TILE_PART_BYTES > SPLIT_PART_BUDGET:
+                s_ -= 1
+            tp.nsplit[li] = s_
+    # wide tiles where a level's merges fill 512 rows and it has two waves of them
+    if geom.head_mode == 0 and compact_mode != "gathered":
+        wide_env = env.get("KVF_SIM_WIDE", "auto")
+        tmw, _, _ = tile_shape(dtype, 0, N.PATH_TC_WIDE)
+        for li, lv in enumerate(plan.levels):
+            if tp.nsplit[li] != 1 or wide_env == "0" or not len(lv.merges) or tp.paired[li]:
+                continue
+            left_min = int((lv.merges[:, 1] - lv.merges[:, 0]).min())
+            nt_w = int(lv.tiling(tmw, tn)[0].shape[0])
+            if wide_env == "1" or (left_min >= tmw and nt_w * U >= 2 * pairs):
+                tp.wide[li] = True
+                tp.nt[li] = nt_w
+    # fused level-1 key norms: every block is an operand row of exactly one level-1 tile
+    if dtype == torch.bfloat16 and nlv and env.get("KVF_FUSE_KNORM", "1") != "0":
+        lv0 = plan.levels[0]
+        m0 = lv0.merges
+        tp.fuse_knorm = bool(
+            len(m0) and tp.nsplit[0] == 1 and not tp.wide[0] and not compacted[0]
+            and (lv0.row_merge >= 0).all()
+            and int((m0[:, 1] - m0[:, 0]).max()) <= tm and int((m0[:, 2] - m0[:, 1]).max()) <= tn)
+    return tp
+
+
+def _simt_tile() -> int:
+    return tile_shape(torch.float64, 0, N.PATH_SIMT)[0]
+
+
 class FusionEngine:
     """Runs fusion of all units of a geometry for one plan (see module doc)."""
 
@@ -233,21 +325,16 @@ class FusionEngine:
         # member counts / segments / absorber list of the current level
         self.level_ws = torch.zeros(int(N.lib().kvf_level_ws_ints(U * NB)), dtype=torch.int32,
                                     device=dev)
-        # compaction of the top levels (tcgen05 path): dead blocks dominate the
-        # upper merges' rectangles, so their alive K rows are staged densely
-        if compact_from == "auto":
-            compact_from = plan.tree_depth - 1 if plan.tree_depth >= 4 else None
-            # very large merges (>= COMPACT_BIG_MERGE blocks) also compact one level lower:
-            # their rectangle cost grows with the merge size while staging grows with the
-            # block count (cfg5 shape, 262,144 blocks per layer: heights 6-8 compacted,
-            # 571 -> 534-547 ms per layer; heights 5-8: 551 ms)
-            if compact_from is not None and compact_from - 1 >= 2:
-                lo = [lv for lv in plan.levels if lv.height == compact_from - 1]
-                if lo and len(lo[0].merges) and int((lo[0].merges[:, 2] - lo[0].merges[:, 0]).min()) >= COMPACT_BIG_MERGE:
-                    compact_from -= 1
-        if path != N.PATH_TC or geom.d % 8 != 0 or self.filter_mode:
-            compact_from = None
+        pairs = 74
+        if path == N.PATH_TC:
+            pairs = max(1, torch.cuda.get_device_properties(self.device).multi_processor_count // 2)
+        # compaction of the top levels (tcgen05 path: dead blocks dominate the upper merges'
+        # rectangles, so their alive K rows are staged densely), paired / split-K / wide
+        # launches per level and the fused level-1 norms: tile_plan (host logic)
+        tp = tile_plan(plan, geom, dtype, path, compact_from, compact_mode, split, pairs)
+        compact_from = tp.compact_from
         self.compact_from = compact_from
+        self.paired, self.nsplit, self.wide, self.fuse_knorm = tp.paired, tp.nsplit, tp.wide, tp.fuse_knorm
         # exact float64 re-score of pairs within RESCORE_BAND of the threshold
         # (tensor-core fp32 accumulation error is ~1e-4 relative at r = 16K)
         self.rescore_cap = RESCORE_CAP if path == N.PATH_TC else 0
@@ -256,76 +343,27 @@ class FusionEngine:
         # hi / lo bf16 split of a float32 pool (kvf_convert_rows), 2 x the pool's elements
         self.filter = (torch.empty(2 * geom.L * NB * geom.E, dtype=torch.bfloat16, device=dev)
                        if self.filter_mode else None)
-        # paired small merges (KVF_SIM_PAIRED): a level whose merge sides all fit one
-        # 128-row box runs two merges per tile on the pair tile's diagonal, each CTA streaming
-        # only its own merge's rows (cfg3 level 1: 128 x 128 merges; cfg1: 64 / 128)
+        # device tile lists of the chosen launches
         self.levels = list(self.pdev.levels)
-        self.paired = [False] * len(self.levels)
-        if path == N.PATH_TC and os.environ.get("KVF_SIM_PAIRED", "1") != "0":
-            for li, lvp in enumerate(plan.levels):
-                compacted = compact_from is not None and lvp.height >= compact_from
-                m_ = lvp.merges
-                if (len(m_) >= 2 and not compacted and int((m_[:, 1] - m_[:, 0]).max()) <= self.tm // 2
-                        and int((m_[:, 2] - m_[:, 1]).max()) <= self.tn // 2):
-                    self.paired[li] = True
-                    self.levels[li] = _paired_level(self.levels[li], self.ppt, self.device)
-        # split-K per level (tcgen05 path): few, long-K tiles (cfg1, CFF) spread over all SMs
-        self.nsplit = [1] * len(self.pdev.levels)
-        self.split_part = self.split_count = None
-        pairs = 74
-        if path == N.PATH_TC:
-            pairs = max(1, torch.cuda.get_device_properties(self.device).multi_processor_count // 2)
-        if path == N.PATH_TC and split:
-            nk = geom.r // 64 * (3 if self.filter_mode else 1)
-            need, tiles_max = 0, 0
-            for li, lv in enumerate(self.levels):
-                compacted = compact_from is not None and plan.levels[li].height >= compact_from
-                if compacted and compact_mode == "gathered":
-                    continue
-                n_tiles = lv["nt"] * U
-                s = choose_split(n_tiles, nk, pairs)
-                while s > 1 and n_tiles * s * _TILE_PART_BYTES > SPLIT_PART_BUDGET:
-                    s -= 1
-                self.nsplit[li] = s
-                if s > 1:
-                    need = max(need, n_tiles * s * _TILE_PART_BYTES)
-                    tiles_max = max(tiles_max, n_tiles)
-            if need:
-                self.split_part = torch.empty(need // 4, dtype=torch.float32, device=dev)
-                self.split_count = torch.zeros(2 * tiles_max, dtype=torch.int32, device=dev)
-        # wide tiles (512 x 256 per CTA pair, KVF_PATH_TC_WIDE) for the levels they fit: the
-        # narrow tile's 128 FLOP per L2->SM byte leaves the tensor pipe ~20% idle on the
-        # crossbar; the wide tile gives up the double-buffered TMEM accumulator for 171
-        self.wide = [False] * len(self.pdev.levels)
-        if path == N.PATH_TC and geom.head_mode == 0 and compact_mode != "gathered":
-            wide_env = os.environ.get("KVF_SIM_WIDE", "auto")
-            tmw, _, _ = tile_shape(dtype, 0, N.PATH_TC_WIDE)
-            pdw = None
-            for li, lvp in enumerate(plan.levels):
-                if self.nsplit[li] != 1 or wide_env == "0" or not len(lvp.merges) or self.paired[li]:
-                    continue
-                left_min = int((lvp.merges[:, 1] - lvp.merges[:, 0]).min())
+        pdw = None
+        for li in range(len(self.levels)):
+            if self.paired[li]:
+                self.levels[li] = _paired_level(self.levels[li], self.ppt, self.device)
+            elif self.wide[li]:
                 if pdw is None:
+                    tmw, _, _ = tile_shape(dtype, 0, N.PATH_TC_WIDE)
                     pdw = _plan_device(plan, tmw, self.tn, self.ppt, self.device)
-                if wide_env == "1" or (left_min >= tmw and pdw.levels[li]["nt"] * U >= 2 * pairs):
-                    self.wide[li] = True
-                    self.levels[li] = pdw.levels[li]
+                self.levels[li] = pdw.levels[li]
+        # split-K partials (fp32 accumulator tiles) and arrival counters
+        self.split_part = self.split_count = None
+        need = max([self.levels[li]["nt"] * U * s_ * _TILE_PART_BYTES
+                    for li, s_ in enumerate(self.nsplit) if s_ > 1], default=0)
+        if need:
+            tiles_max = max(self.levels[li]["nt"] * U for li, s_ in enumerate(self.nsplit) if s_ > 1)
+            self.split_part = torch.empty(need // 4, dtype=torch.float32, device=dev)
+            self.split_count = torch.zeros(2 * tiles_max, dtype=torch.int32, device=dev)
         max_nt = max([lv["nt"] for lv in self.levels], default=1)
         self.partials = torch.empty((U, max(max_nt * self.ppt, 1), 5), dtype=torch.float64, device=dev)
-        # key norms fused into the first level's similarity launch (KVF_SIM_WRITE_NORMS):
-        # every block is an operand row of exactly one level-1 tile when every row takes part
-        # in a level-1 merge whose sides fit one narrow tile; saves the K pass of the norms
-        # (17 GB read per cfg2 step)
-        self.fuse_knorm = False
-        if (path == N.PATH_TC and dtype == torch.bfloat16 and plan.levels
-                and os.environ.get("KVF_FUSE_KNORM", "1") != "0"):
-            lv0 = plan.levels[0]
-            m0 = lv0.merges
-            compact0 = compact_from is not None and lv0.height >= compact_from
-            self.fuse_knorm = bool(
-                len(m0) and self.nsplit[0] == 1 and not self.wide[0] and not compact0
-                and (lv0.row_merge >= 0).all()
-                and int((m0[:, 1] - m0[:, 0]).max()) <= self.tm and int((m0[:, 2] - m0[:, 1]).max()) <= self.tn)
         self.shadow = self.sidx = self.scount = None
         self.shadow_cap = 0
         if self.exact:
