@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -719,6 +720,11 @@ def ours_main(args):
             except Exception as exc:  # reported, never fatal
                 out["configs"][name] = {"error": str(exc)[-400:]}
             torch.cuda.empty_cache()
+        try:  # chunked prefill over a CFF-fused context (computation reuse)
+            out["configs"]["cff_prefill"] = bench_cff_prefill(dev, torch)
+        except Exception as exc:  # reported, never fatal
+            out["configs"]["cff_prefill"] = {"error": str(exc)[-400:]}
+        torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -1049,6 +1055,88 @@ def bench_cfg5_layer(dev, torch, steps=2, warmup=1):
     }
     del K0, V0, Kw, Vw, eng, st
     torch.cuda.empty_cache()
+    return res
+
+
+def bench_cff_prefill(dev, torch, B=4, p=1024, chunk=7, steps=10):
+    """Chunked prefill of the last 2K-token chunk of 4 requests x 16K (Llama-3-8B layer shape,
+    32 query / 8 KV heads) over their CFF-fused earlier chunks: each fused block's scores are
+    computed once for all the slots that share it (`chunk_prefill(dedup=True)`) vs once per
+    slot (same kernel, dedup off), with flash-attn over the unfused keys as a library
+    reference point. Parity: dedup vs per-slot outputs, and a float64 check of a slice."""
+    import paper_2601_03067_b200 as K
+    from paper_2601_03067_b200.workload import synthetic_kv
+
+    L, t, h, d, Hq, cb = 1, 16, 8, 128, 32, 128
+    Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=5, variant="cff", device=dev)
+    K0, V0 = Kt.clone(), Vt.clone()
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    st = K.fuse_chunks(cache, K.FusionConfig(threshold=0.8, variant="cff"), cb * t, in_place=True,
+                       keep_samples=False)[0].fused.state
+    Tq = cb * t
+    gen = torch.Generator(device=dev).manual_seed(11)
+    q = torch.randn((B, Tq, Hq, d), device=dev, dtype=torch.bfloat16, generator=gen)
+    order = K.state_decode_schedule(st, 0, B, p).order[0]
+    prev = chunk * cb
+    tab = st.table[0].view(B, p)[:, :prev]
+    uniq = int(sum(len(torch.unique(r)) for r in tab))
+    out = torch.empty((B, Tq, Hq, d), dtype=torch.float32, device=dev)
+
+    def timeit(fn):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / steps
+
+    t_dedup = timeit(lambda: K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=True, out=out))
+    t_slot = timeit(lambda: K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=False, out=out))
+    a = K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=True)
+    b = K.chunk_prefill(q, st, 0, B, p, cb, chunk, order=order, dedup=False)
+    # float64 check: request 0, query head 0, 16 query positions, against the refolded fused keys
+    # (what the reference's paged_attention reads through the remapped table, core.py:285-305)
+    G = Hq // h
+    kv_h = 0
+    phys = st.table[0].view(B, p)[0, : (chunk + 1) * cb].long()
+    ks = st.k_scale[0].view(B, p)[0, : (chunk + 1) * cb].double()
+    vs = st.v_scale[0].view(B, p)[0, : (chunk + 1) * cb].double()
+    Kr = (st.pool_k.view(-1, t, h, d)[phys, :, kv_h].double() * ks[:, None, None]).reshape(-1, d)
+    Vr = (st.pool_v.view(-1, t, h, d)[phys, :, kv_h].double() * vs[:, None, None]).reshape(-1, d)
+    pos = torch.arange(0, Tq, Tq // 16, device=dev)
+    err = 0.0
+    for i in pos.tolist():
+        qi = q[0, i, 0].double()
+        n = prev * t + i + 1  # causal: the earlier chunks and this chunk up to position i
+        lg = (Kr[:n] @ qi) / math.sqrt(d)
+        pr = torch.softmax(lg, 0)
+        ref = pr @ Vr[:n]
+        err = max(err, float((a[0, i, 0].double() - ref).abs().max()))
+    flops = 4.0 * B * Hq * Tq * (prev * t + Tq / 2) * d  # dense causal attention equivalent
+    res = {"workload": "cff_chunked_prefill_llama3_8b_4x16k_chunk2k", "unit": "ms",
+           "ms_dedup": t_dedup, "ms_per_slot": t_slot, "speedup_dedup": t_slot / t_dedup,
+           "earlier_slots": B * prev, "earlier_unique_blocks": uniq,
+           "dense_equivalent_tflops_dedup": flops / (t_dedup / 1e3) / 1e12,
+           "parity": {"max_abs_dedup_vs_per_slot": float((a - b).abs().max()),
+                      "max_abs_vs_float64_refold": err,
+                      "note": "request 0, query head 0 (KV head 0, GQA 4), 16 query positions of the chunk"},
+           "config": {"B": B, "ctx": p * t, "chunk_tokens": Tq, "chunk": chunk, "Hq": Hq, "kv_heads": h,
+                      "d": d, "threshold": 0.8, "timing": f"CUDA events over {steps} calls"},
+           "section": "SURVEY §8f rank 2 (computation reuse of CFF-fused blocks in chunked prefill)"}
+    try:  # library reference point (not our kernel): dense causal attention over the unfused keys
+        from flash_attn import flash_attn_func
+
+        tk = (chunk + 1) * Tq
+        kf = K0[0].view(B, p * t, h, d)[:, :tk]
+        vf = V0[0].view(B, p * t, h, d)[:, :tk]
+        res["ms_flash_attn_unfused"] = timeit(lambda: flash_attn_func(q, kf, vf, causal=True))
+    except Exception as exc:  # library optional
+        res["ms_flash_attn_unfused"] = None
+        res["flash_attn_note"] = str(exc)[:120]
+    del Kt, Vt, K0, V0, cache, st, q, out, a, b
     return res
 
 
