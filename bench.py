@@ -725,6 +725,11 @@ def ours_main(args):
         except Exception as exc:  # reported, never fatal
             out["configs"]["cff_prefill"] = {"error": str(exc)[-400:]}
         torch.cuda.empty_cache()
+        try:  # fused-pool storage / hand-off
+            out["configs"]["fused_pool_io"] = bench_fused_pool_io(dev, torch)
+        except Exception as exc:  # reported, never fatal
+            out["configs"]["fused_pool_io"] = {"error": str(exc)[-400:]}
+        torch.cuda.empty_cache()
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -1137,6 +1142,61 @@ def bench_cff_prefill(dev, torch, B=4, p=1024, chunk=7, steps=10):
         res["ms_flash_attn_unfused"] = None
         res["flash_attn_note"] = str(exc)[:120]
     del Kt, Vt, K0, V0, cache, st, q, out, a, b
+    return res
+
+
+def bench_fused_pool_io(dev, torch, steps=3):
+    """One cfg2 layer (64 requests x 4K, BFF-fused): compaction to the live blocks on the
+    device (kvf_alive_rank + kvf_stage_rows + kvf_remap_ids), the KVFF v2 file round trip
+    (save_fused / load_fused) and the bytes a prefill -> decode hand-off moves, fused vs
+    unfused; the reloaded layer decodes bitwise like the original."""
+    import tempfile
+
+    from paper_2601_03067_b200.compact import (compact_cache, compact_decode_schedule, decode_compact,
+                                               load_fused, save_fused)
+    from paper_2601_03067_b200.engine import FusionEngine, Geometry
+    from paper_2601_03067_b200.schedule import bff_plan
+    from paper_2601_03067_b200.workload import synthetic_kv
+
+    L, B, p, t, h, d = 1, 64, 256, 16, 8, 128
+    K0, V0 = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=GPU_SEED, device=dev, layers=[0])
+    eng = FusionEngine(Geometry(L, B * p, t, h, d, 0), bff_plan(B, p, None), torch.bfloat16, dev)
+    st = eng.run(K0.reshape(-1), V0.reshape(-1), 0.8)
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        cl = compact_cache(st, B, p)[0]
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms_compact = min(times)
+    unfused = 2 * B * p * t * h * d * 2
+    with tempfile.TemporaryDirectory(dir="/dev/shm" if os.path.isdir("/dev/shm") else None) as td:
+        path = os.path.join(td, "layer.kvff")
+        t0 = time.perf_counter()
+        nbytes = save_fused(path, [cl])
+        t_save = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        back = load_fused(path, device=dev)[0]
+        torch.cuda.synchronize()
+        t_load = time.perf_counter() - t0
+    q = torch.randn((B, 32, d), device=dev, dtype=torch.bfloat16)
+    o1, _ = decode_compact(q, cl, compact_decode_schedule(cl))
+    o2, _ = decode_compact(q, back, compact_decode_schedule(back))
+    res = {"workload": "bff_llama3_8b_layer_bs64_ctx4k_compact_kvff2", "unit": "GB",
+           "unfused_layer_gb": unfused / 1e9, "fused_layer_gb": cl.nbytes / 1e9, "kvff2_file_gb": nbytes / 1e9,
+           "bytes_ratio": unfused / cl.nbytes, "live_blocks": cl.n_live, "blocks": B * p,
+           "ms_compact_device": ms_compact,
+           "compact_gbs": 2 * cl.n_live * t * h * d * 2 * 2 / (ms_compact / 1e3) / 1e9,
+           "s_save_host": t_save, "s_load_host_to_device": t_load,
+           "reload_decode_bitwise_equal": bool(torch.equal(o1, o2)),
+           "note": "compaction reads and writes the live K and V rows (compact_gbs counts both); the file "
+                   "round trip goes through host memory (/dev/shm); a prefill -> decode hand-off "
+                   "(compact.send_layer / recv_layer) moves fused_layer_gb instead of unfused_layer_gb",
+           "section": "SURVEY §8f rank 4 (fused-pool serialization / transfer)"}
+    del K0, V0, eng, st, cl, back
     return res
 
 
