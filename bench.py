@@ -725,6 +725,11 @@ def ours_main(args):
         except Exception as exc:  # reported, never fatal
             out["configs"]["cff_prefill"] = {"error": str(exc)[-400:]}
         torch.cuda.empty_cache()
+        try:  # the threshold controller on device-computed statistics
+            out["configs"]["adaptive_threshold"] = bench_adaptive_threshold(dev, torch)
+        except Exception as exc:  # reported, never fatal
+            out["configs"]["adaptive_threshold"] = {"error": str(exc)[-400:]}
+        torch.cuda.empty_cache()
         try:  # fused-pool storage / hand-off
             out["configs"]["fused_pool_io"] = bench_fused_pool_io(dev, torch)
         except Exception as exc:  # reported, never fatal
@@ -1143,6 +1148,52 @@ def bench_cff_prefill(dev, torch, B=4, p=1024, chunk=7, steps=10):
         res["flash_attn_note"] = str(exc)[:120]
     del Kt, Vt, K0, V0, cache, st, q, out, a, b
     return res
+
+
+def bench_adaptive_threshold(dev, torch):
+    """The reference's threshold controller (fusion.py:418-465) over device fusion runs:
+    tune_threshold (target-compression) on the cfg2 cache with every iteration a full
+    32-layer fusion, and one percentile step whose quantile is computed on the device
+    (kvf_quantile, exact radix select) from the cfg1 run's samples, against np.quantile."""
+    import numpy as np
+
+    import paper_2601_03067_b200 as K
+    from paper_2601_03067_b200.fusion import device_quantile
+    from paper_2601_03067_b200.workload import synthetic_kv
+
+    c = CONFIGS["cfg2"]
+    L, B, p, t, h, d = c["L"], c["B"], c["p"], c["t"], c["h"], c["d"]
+    Kt, Vt = synthetic_kv(L, B, p, t, h, d, dtype=torch.bfloat16, seed=GPU_SEED, device=dev)
+    cache = K.PagedKvCache(K.CacheDims(B=B, p=p, t=t, h=h, d=d, L=L), Kt, Vt)
+    policy = K.AdaptPolicy(mode="target-compression", target=1.5, step=0.02, min_threshold=0.5,
+                           max_threshold=0.95)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    thr, hist = K.tune_threshold(cache, K.FusionConfig(threshold=0.8), policy, rel_tol=0.05)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    del cache, Kt, Vt
+    torch.cuda.empty_cache()
+    c1 = CONFIGS["cfg1"]
+    K1, V1 = synthetic_kv(c1["L"], c1["B"], c1["p"], c1["t"], c1["h"], c1["d"], dtype=torch.float32,
+                          seed=GPU_SEED, device=dev)
+    cache1 = K.PagedKvCache(K.CacheDims(B=c1["B"], p=c1["p"], t=c1["t"], h=c1["h"], d=c1["d"], L=c1["L"]),
+                            K1, V1)
+    outs = K.fuse_batch(cache1, K.FusionConfig(threshold=0.8), keep_samples=True)
+    rep = K.FusionReport.aggregate([o.report for o in outs])
+    pol = K.AdaptPolicy(mode="percentile", target=0.02, step=0.01, min_threshold=0.5, max_threshold=0.99)
+    qd = device_quantile(rep.device_samples(), 1.0 - pol.target)
+    qh = float(np.quantile(rep.similarity_samples, 1.0 - pol.target))
+    return {"workload": "tune_threshold_cfg2_target_cr_1.5", "unit": "s",
+            "iterations": len(hist), "final_threshold": thr, "final_cr": hist[-1][1] if hist else None,
+            "trajectory": [[round(a, 4), round(b, 4)] for a, b in hist],
+            "s_total": wall, "s_per_iteration": wall / max(1, len(hist)),
+            "percentile_step": {"samples": int(rep.similarity_samples.size), "device_quantile": qd,
+                                "np_quantile": qh, "bitwise_equal": qd == qh,
+                                "new_threshold": K.adapt_threshold(pol, rep, 0.8)},
+            "note": "each iteration fuses all 32 cfg2 layers through the public fuse_batch (a copy of the "
+                    "cache, reports built from device counters); the percentile quantile never leaves the GPU",
+            "section": "SURVEY §8f rank 3 (on-device adaptive threshold)"}
 
 
 def bench_fused_pool_io(dev, torch, steps=3):
