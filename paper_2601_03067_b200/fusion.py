@@ -281,17 +281,43 @@ class FusionReport:
             layer=-1,
             blocks_before=sum(r.blocks_before for r in reports),
             blocks_after=sum(r.blocks_after for r in reports),
-            fused_events=[e for r in reports for e in r.fused_events],
+            fused_events=None,  # concatenated on first access (_AggregateLazy)
             merge_calls=sum(r.merge_calls for r in reports),
             tree_depth=max((r.tree_depth for r in reports), default=0),
             similarity_samples=samp,
             merge_records=None if on_device else [m for r in reports for m in r.merge_records],
         )
+        inner = None
         if on_device:
-            out._lazy = _DeviceParts([t for p in parts for t in p], reports)
+            inner = _DeviceParts([t for p in parts for t in p], reports)
         elif samp is None:
-            out._lazy = _NoSamples()
+            inner = _NoSamples()
+        out._lazy = _AggregateLazy(reports, inner)
         return out
+
+
+class _AggregateLazy:
+    """Aggregate report: the events of the parts are concatenated on first access (a
+    threshold controller reading only the aggregate CR never builds the ~260K event
+    objects of a cfg2 cache); samples / records come from `inner` when given."""
+
+    def __init__(self, reports, inner):
+        self.reports = reports
+        self.inner = inner
+        self.has_samples = inner.has_samples if inner is not None else True
+
+    def events(self):
+        return [e for r in self.reports for e in r.fused_events]
+
+    def records(self):
+        return self.inner.records() if self.inner is not None else []
+
+    def samples(self):
+        return self.inner.samples()
+
+    def device_samples(self):
+        fn = getattr(self.inner, "device_samples", None)
+        return fn() if fn is not None else None
 
 
 class _DeviceParts:
