@@ -1169,6 +1169,10 @@ def bench_adaptive_threshold(dev, torch):
                            max_threshold=0.95)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
+    K.tune_threshold(cache, K.FusionConfig(threshold=0.8), policy, rel_tol=0.05)  # cold: allocations
+    torch.cuda.synchronize()
+    cold = time.perf_counter() - t0
+    t0 = time.perf_counter()
     thr, hist = K.tune_threshold(cache, K.FusionConfig(threshold=0.8), policy, rel_tol=0.05)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
@@ -1187,7 +1191,7 @@ def bench_adaptive_threshold(dev, torch):
     return {"workload": "tune_threshold_cfg2_target_cr_1.5", "unit": "s",
             "iterations": len(hist), "final_threshold": thr, "final_cr": hist[-1][1] if hist else None,
             "trajectory": [[round(a, 4), round(b, 4)] for a, b in hist],
-            "s_total": wall, "s_per_iteration": wall / max(1, len(hist)),
+            "s_total": wall, "s_per_iteration": wall / max(1, len(hist)), "s_total_cold_first_call": cold,
             "percentile_step": {"samples": int(rep.similarity_samples.size), "device_quantile": qd,
                                 "np_quantile": qh, "bitwise_equal": qd == qh,
                                 "new_threshold": K.adapt_threshold(pol, rep, 0.8)},
