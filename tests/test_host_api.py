@@ -166,3 +166,24 @@ def test_stream_chunks_cover_layers_in_order():
         assert sizes == sorted(sizes, reverse=True)
         if L > 1:
             assert sizes[-1] == 1
+
+
+def test_aggregate_events_lazy_and_equal():
+    """FusionReport.aggregate concatenates the parts' events only when they are read, and
+    they equal the reference's eager concatenation (fusion.py:158-171)."""
+    from paper_2601_03067_b200.fusion import FusionEvent
+
+    parts = [
+        FusionReport(layer=i, blocks_before=8, blocks_after=8 - i, merge_calls=3, tree_depth=2,
+                     fused_events=[FusionEvent((0, k), ((1, k),)) for k in range(i)],
+                     similarity_samples=np.arange(i, dtype=np.float64))
+        for i in range(4)
+    ]
+    agg = FusionReport.aggregate(parts)
+    assert agg._events is None  # not built by aggregate itself
+    assert agg.compression_ratio == 32 / (32 - 6) and agg.fused_blocks == 6
+    assert agg._events is None  # CR and fused block count do not need the events
+    assert agg.fused_events == [e for r in parts for e in r.fused_events]
+    assert agg.merge_calls == 12 and agg.tree_depth == 2 and agg.layer == -1
+    np.testing.assert_array_equal(agg.similarity_samples, np.concatenate([np.arange(i) for i in range(4)]))
+    assert agg.to_dict()["fused_events"][0] == [[0, 0], [[1, 0]]]
